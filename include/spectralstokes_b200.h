@@ -1,0 +1,142 @@
+/*
+ * spectralstokes_b200 — C ABI of the B200-native spectral-Stokes hot path (libss_b200.so).
+ *
+ * The reference (arXiv 2009.06725's Python package `spectralstokes`, mounted at
+ * /root/reference/pkg) has no FFI: its boundary is the Python API re-exported in
+ * pkg/src/spectralstokes/__init__.py:10-46.  Each entry point below replaces the reference
+ * function named beside it; the Python package paper_2009_06725_b200 binds them with ctypes
+ * (INTEGRATION.md shows the binding a reference maintainer would add).
+ *
+ * Conventions
+ *   - every function returns 0 (SS_OK) or an error code; nothing throws across the ABI;
+ *     ss_last_error() returns the message.  Codes: 1 = bad argument (ValueError),
+ *     2 = mesh error (MeshError), 3 = CUDA/driver (DeviceError), 4 = misuse (RuntimeError).
+ *   - complex128 arrays are interleaved {re, im} doubles;
+ *   - pointers named *_dev are device pointers owned by the caller; *_host are host pointers;
+ *   - stream is a cudaStream_t (NULL = legacy default stream);
+ *   - per-mode vectors are mode-major with a leading dimension `ld` (complex elements).
+ *   - the library owns only its opaque handles (ss_pattern, ss_krylov) and never frees caller memory.
+ */
+#ifndef SPECTRALSTOKES_B200_H
+#define SPECTRALSTOKES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ss_pattern ss_pattern; /* mesh numbering + symbolic pattern + device operator  */
+typedef struct ss_krylov ss_krylov;   /* batched GMRES workspace (basis, Hessenberg, state)   */
+
+const char* ss_last_error(void);
+int ss_version(void);
+int64_t ss_launch_count(void); /* kernels launched by this library so far (graph nodes counted) */
+
+/* Reference tables Mref(nv x nv), sref(nv x nv x dim x dim), tref(nv x dim x (dim+1)) of the degree-4
+ * rules; replaces reference_shapes + the einsum contractions (assembly.py:115-128,169,182,236). */
+int ss_reference_tables(int dim, double* mref, double* sref, double* tref);
+
+/* Symbolic reduced pattern, DOF maps, element->slot maps and element colouring.
+ * Replaces the pattern half of assemble_mode_system (assembly.py:424-479: kron/bmat/COO->CSR,
+ * vel_dof/pres_dof numbering at 455-475, reduction a_full[free][:, free] at 477-479).
+ * vel_conn: n_elements x (6|10) int64, fixed_mask: n_vel_nodes uint8 (dirichlet/wall nodes,
+ * constrained_velocity_nodes assembly.py:392-400), pinned_pressure per assembly.py:460-464. */
+int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertices, int64_t n_elements,
+                      const int64_t* vel_conn_host, const uint8_t* fixed_mask_host, int pinned_pressure,
+                      int device, ss_pattern** out);
+void ss_pattern_destroy(ss_pattern* p);
+/* info[16]: n, nnz, n_free_nodes, n_free_pressures, nnz_node, nnz_vp, nnz_pv, n_colors,
+ *           nnz_lift, nnz_lift_t, dim, pinned, element-map bytes, n_vel_nodes, n_vertices, n_elements */
+int ss_pattern_info(const ss_pattern* p, int64_t* info);
+/* Bit-exact reduced CSR pattern (= ComplexSaddleSystem.matrix.indptr/.indices, assembly.py:479).
+ * indices may be NULL to obtain indptr only. */
+int ss_pattern_export(const ss_pattern* p, int32_t* indptr_host, int32_t* indices_host);
+/* ComplexSaddleSystem.vel_dof (n_vel_nodes x dim) and .pres_dof (n_vertices) (assembly.py:319-320). */
+int ss_pattern_dof_maps(const ss_pattern* p, int64_t* vel_dof_host, int64_t* pres_dof_host);
+
+/* Device element assembly of S' = mu*S, M' = rho*M and D once per mesh, colour by colour,
+ * atomic-free.  Replaces _element_geometry + assemble_{mass,stiffness}_scalar +
+ * assemble_divergence (assembly.py:151-246).  vertex_nodes_host: n_vertices x dim.
+ * Returns 2 (MeshError) for a degenerate Jacobian (assembly.py:156-157). */
+int ss_assemble(ss_pattern* p, const double* vertex_nodes_host, double density, double viscosity, void* stream);
+/* Values of the reduced matrix at frequency omega in the exported CSR order
+ * (= ComplexSaddleSystem.matrix.data, assembly.py:425-430,479).  data_dev: nnz complex. */
+int ss_export_values(const ss_pattern* p, double omega, double* data_dev, void* stream);
+
+/* Consistent traction load on a patch, accumulated into load_host (n_vel_nodes x dim complex).
+ * Replaces boundary_traction_load/_surface_load (assembly.py:249-305).
+ * h_kind 0: uniform (dim complex), 1: per face (n_faces x dim), 2: nodal (n_vel_nodes x dim). */
+int ss_surface_load(int dim, int64_t n_vel_nodes, const double* nodes_host, int64_t n_faces,
+                    const int64_t* face_conn_host, int h_kind, const double* h_host, double* load_host);
+/* rhs_b = load_b[free] - A(omega_b)[free, fixed] g_b[fixed] for nb modes
+ * (assembly.py:432-478).  load_dev / g_dev: nb x n_vel_nodes*dim complex (NULL = 0);
+ * omegas_dev: nb doubles; rhs_dev: nb x ld complex. */
+int ss_rhs_batched(const ss_pattern* p, int nb, const double* omegas_dev, const double* load_dev,
+                   const double* g_dev, double* rhs_dev, int64_t ld, void* stream);
+/* Mode-batched SpMV Y_b = s_b .* (A(omega_b) X_b), s = Jacobi scale if jacobi else 1.
+ * Replaces `matrix @ q` / `scale * (matrix @ q)` (krylov.py:94,108,155; assembly.py:362). */
+int ss_spmv_batched(const ss_pattern* p, int nb, const double* omegas_dev, const double* x_dev,
+                    double* y_dev, int64_t ld, int jacobi, void* stream);
+/* Algorithmic bytes of one ss_spmv_batched call over nb modes (roofline numerator). */
+int64_t ss_spmv_bytes(const ss_pattern* p, int nb);
+/* True relative residuals ||b - A x||/||b|| (||A x|| if b = 0) per mode (ComplexSaddleSystem.residual_norm,
+ * assembly.py:357-362).  out_host: nb doubles. */
+int ss_residual_norms(const ss_pattern* p, int nb, const double* omegas_dev, const double* rhs_dev, const double* x_dev,
+                      int64_t ld, double* out_host, void* stream);
+/* Jacobi scale vectors 1/diag (1 where diag = 0) per mode (jacobi_precondition, krylov.py:49-60). */
+int ss_jacobi(const ss_pattern* p, int nb, const double* omegas_dev, double* scale_dev, int64_t ld, void* stream);
+/* Reduced solutions -> nodal velocity (nb x n_vel_nodes*dim) and pressure (nb x n_vertices),
+ * Dirichlet values from g_dev (ComplexSaddleSystem.expand, assembly.py:338-346). */
+int ss_expand(const ss_pattern* p, int nb, const double* x_dev, int64_t ld, const double* g_dev,
+              double* u_dev, double* p_dev, void* stream);
+
+/* Batched restarted GMRES workspace on the structured operator of `p` (gmres, krylov.py:63-164). */
+int ss_krylov_create_saddle(const ss_pattern* p, int max_batch, int restart, int64_t hist_cap, ss_krylov** out);
+/* Same on an arbitrary complex CSR matrix (drop-in gmres(matrix, rhs, ...) for any scipy matrix).
+ * vals_host: nvals x nnz complex (nvals = 1 shared or one set per mode); scale_host: optional
+ * nvals x n complex left preconditioner (krylov.py:63 `scale`); jacobi_from_diag != 0 (and no
+ * scale_host) computes 1/diag on the device (jacobi_precondition, krylov.py:49-60). */
+int ss_krylov_create_csr(int device, int n, int64_t nnz, const int32_t* indptr_host, const int32_t* indices_host,
+                         int nvals, const double* vals_host, const double* scale_host, int jacobi_from_diag,
+                         int max_batch, int restart, int64_t hist_cap, ss_krylov** out);
+void ss_krylov_destroy(ss_krylov* k);
+/* info[10]: n, ld, restart, n_segments, segment_rows, spmv_blocks, max_batch, ticks_per_graph,
+ *           pass shared-memory bytes, kind */
+int ss_krylov_info(const ss_krylov* k, int64_t* info);
+/* The workspace's own RHS and X buffers (nb x ld complex, device) for zero-copy callers. */
+int ss_krylov_buffers(ss_krylov* k, double** rhs_dev, double** x_dev, int64_t* ld);
+/* Solve nb modes to relative tolerance tol (krylov.py:63-164 semantics per mode).
+ * rhs_dev/x_dev (nb x ld_in complex) may be NULL to use the workspace buffers in place;
+ * use_x0 != 0 starts from x (krylov.py:79).  out_int[6*b+{iterations, converged, breakdown, phase, history length, zero rhs}],
+ * out_dbl[4*b+{true residual at last cycle end, last estimate, ||b||, final target}]. */
+int ss_krylov_solve(ss_krylov* k, int nb, const double* omegas_host, const int* sets_host, const double* rhs_dev,
+                    double* x_dev, int64_t ld_in, int use_x0, double tol, int64_t maxiter, int jacobi,
+                    void* stream, int64_t* out_int, double* out_dbl);
+/* Per-iteration preconditioned residual estimates of mode b (SolveReport.residual_history). */
+int ss_krylov_history(const ss_krylov* k, int mode, int64_t count, double* out_host);
+/* Ticks and kernel launches of the last solve. */
+int ss_krylov_last_stats(const ss_krylov* k, int64_t* ticks, int64_t* launches);
+/* True relative residuals ||b - A x||/||b|| of the workspace's X (residual_norm, assembly.py:357-362). */
+int ss_krylov_residuals(ss_krylov* k, int nb, void* stream, double* out_host);
+/* Copy nb vectors caller <-> workspace (dir 0: buf -> RHS, 1: buf -> X, 2: X -> buf). */
+int ss_krylov_copy(ss_krylov* k, int nb, int dir, double* buf_dev, int64_t ld_in, void* stream);
+/* Jacobi scale (1/diag) of a CSR workspace's value set (jacobi_precondition on a matrix, krylov.py:49-60). */
+int ss_krylov_csr_scale(const ss_krylov* k, int set, double* scale_host);
+/* Instrumented solve (no graph; CUDA events between kernels) for the roofline: per kernel kind
+ * (0 spmv, 1 c = Q^H w, 2 w -= Qc & c2 = Q^H w, 3 w -= Q c2 & ||w||, 4 x += Q y) the summed device time
+ * ms_out[5], algorithmic bytes bytes_out[5] (basis passes only) and launch counts launches_out[5]. */
+int ss_krylov_profile(ss_krylov* k, int nb, const double* omegas_host, double tol, int64_t maxiter, int jacobi,
+                      void* stream, double* ms_out, int64_t* bytes_out, int64_t* launches_out);
+/* Isolated Gram-Schmidt pass timing (which = 1: c = Q^H w; 2: fused w -= Qc, c2 = Q^H w). */
+int ss_krylov_bench_pass(ss_krylov* k, int nb, int kidx, int which, int reps, void* stream, float* ms, int64_t* bytes);
+
+/* out[t][i] = sum_b Re(fields_b[i] * phases[b][t]) for nt samples (reconstruct, spectral.py:308-317).
+ * fields_dev: nb x n complex; phases_dev: nb x nt complex; out_dev: nt x n doubles. */
+int ss_reconstruct(int nb, int nt, int64_t n, const double* fields_dev, const double* phases_dev, double* out_dev,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

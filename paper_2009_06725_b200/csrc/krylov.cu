@@ -1,0 +1,1118 @@
+// Mode-batched, device-resident restarted GMRES(m) with left Jacobi preconditioning and CGS2.
+//
+// Restates the reference solver gmres (pkg/src/spectralstokes/krylov.py:63-164) for a batch of
+// independent modes.  Semantics kept exactly (SURVEY.md §8a'): same restart, classical Gram-
+// Schmidt with one reorthogonalisation (H column = c + c2), complex Givens rotations, the
+// est <= tol*||s.b|| inner exit, the true-residual re-check at every cycle end, the x0.25 target
+// tightening, happy/denominator breakdowns and maxiter counted in inner iterations.  Allowed
+// re-associations only: w -= Qc fused with c2 = Q^H w (3 basis passes instead of 4), deferred
+// 1/||w|| scaling of stored basis vectors, mode-major storage.
+//
+// Execution model: each mode carries a small device state machine (ModeCtl.phase).  One "tick"
+// is a fixed sequence of five kernels over the whole batch, captured in a CUDA graph:
+//   spmv   INNER/START: w = s.(A q_k)          RESID: t = b - A x, r = s.t, norms, cycle decisions
+//   passA  INNER: c  = Q^H w                    (partials per segment, last CTA reduces)
+//   passB  INNER: w -= Q c ; c2 = Q^H w         (one read of Q for both)
+//   passC  INNER: w -= Q c2 ; Q[k+1] = w ; ||w|| -> last CTA: Givens, estimate, exit tests,
+//                 triangular solve at cycle end
+//   passX  XUPDATE: x += Q y
+// Every state change is made by the last CTA of a mode in a kernel, so all CTAs of a mode see a
+// consistent phase.  The reduction structure of a mode depends only on (n, k, restart), never on
+// which other modes share the batch: per-mode results are bitwise invariant under batching and
+// mode order (the reference's test_spectral.py:187-205 contract).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include "ss_common.h"
+#include "ss_pattern.h"
+#include "ss_spmv.cuh"
+
+enum Phase : int { PH_IDLE = 0, PH_RESID = 1, PH_START = 2, PH_INNER = 3, PH_XUPDATE = 4, PH_DONE = 5 };
+
+struct ModeCtl {
+  int phase, k, iters, maxiter;
+  int restart, breakdown, first, converged;
+  int zero_x, set, hist_len, pad1;
+  double beta, target, bnorm, tol;
+  double omega, true_res, gk_last, est;
+};
+
+constexpr int PT = 256;        // threads per CTA for every Krylov kernel
+constexpr int SPMV_TPW = 8;    // warp tasks (rows) per warp in the tick SpMV
+
+struct KArgs {
+  int kind;                    // 0 saddle, 1 csr
+  int nb, n, restart, jcap;
+  int64_t ld;
+  int nseg, seg_rows;          // pass segmentation (depends on n only)
+  int nsb;                     // spmv blocks per mode
+  int cap;                     // double2 capacity of one smem stage
+  int jacobi;
+  int64_t hist_cap;
+  SsOperatorDev op;
+  SsCsrDev csr;
+  ModeCtl* ctl;
+  double2 *Q, *W, *X, *RHS;
+  double* qs;                  // [b][jcap] scale of raw basis vectors
+  double2 *H, *G, *CS, *SN, *C1, *C2, *Y;
+  double2* part;               // [b][nseg][jcap] pass partials
+  double2* spart;              // [b][nsb] spmv partials (x: ||t||^2, y: ||r||^2)
+  int* counters;               // [b][8]
+  int* n_done;
+  double* hist;                // [b][hist_cap]
+  unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
+};
+
+__device__ __forceinline__ double2* qvec(const KArgs& a, int b, int j) {
+  return a.Q + ((size_t)b * a.jcap + j) * a.ld;
+}
+
+// Last-CTA election: returns true in every thread of the CTA that finished last for this mode.
+__device__ __forceinline__ bool last_cta(const KArgs& a, int b, int which, int total, int* sflag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(a.counters + b * 8 + which, 1);
+    *sflag = (t == total - 1);
+    if (*sflag) a.counters[b * 8 + which] = 0;
+  }
+  __syncthreads();
+  const bool last = *sflag;
+  if (last) __threadfence();
+  return last;
+}
+
+__device__ __forceinline__ void mark_done(const KArgs& a, ModeCtl* c, int converged) {
+  c->phase = PH_DONE;
+  c->converged = converged;
+  atomicAdd(a.n_done, 1);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Row scale s_i (Jacobi) for either operator kind.
+// ------------------------------------------------------------------------------------------------
+template <int DIM>
+__device__ __forceinline__ double2 row_scale(const KArgs& a, int b, int row, double om) {
+  if (!a.jacobi) return make_double2(1.0, 0.0);
+  if (a.kind == 0) return row < a.op.nfv ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
+  return a.csr.scale ? a.csr.scale[(size_t)(a.csr.nvals > 1 ? b : 0) * a.csr.n + row] : make_double2(1.0, 0.0);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Init: ||b||, target = tol*||s.b||; phase RESID (krylov.py:71-80).
+// ------------------------------------------------------------------------------------------------
+template <int DIM>
+__global__ void __launch_bounds__(PT) k_init(KArgs a) {
+  __shared__ double red[2][PT];
+  __shared__ int sflag;
+  const int b = blockIdx.x / a.nseg, s = blockIdx.x % a.nseg;
+  if (b >= a.nb) return;
+  ModeCtl* c = a.ctl + b;
+  const double om = c->omega;
+  const double2* rhs = a.RHS + (size_t)b * a.ld;
+  const int r0 = s * a.seg_rows, r1 = min((int64_t)(s + 1) * a.seg_rows, (int64_t)a.n);
+  double bb = 0, sb = 0;
+  for (int i = r0 + threadIdx.x; i < r1; i += PT) {
+    const double2 v = rhs[i];
+    bb += cabs2(v);
+    sb += cabs2(cmul(row_scale<DIM>(a, b, i, om), v));
+  }
+  red[0][threadIdx.x] = bb;
+  red[1][threadIdx.x] = sb;
+  __syncthreads();
+  for (int o = PT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + o];
+      red[1][threadIdx.x] += red[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  double2* part = a.part + ((size_t)b * a.nseg) * a.jcap;
+  if (threadIdx.x == 0) part[(size_t)s * a.jcap] = make_double2(red[0][0], red[1][0]);
+  if (!last_cta(a, b, 5, a.nseg, &sflag)) return;
+  if (threadIdx.x == 0) {
+    double t0 = 0, t1 = 0;
+    for (int q = 0; q < a.nseg; ++q) {
+      const double2 v = __ldcg(part + (size_t)q * a.jcap);
+      t0 += v.x;
+      t1 += v.y;
+    }
+    c->bnorm = sqrt(t0);
+    c->k = 0;
+    c->iters = 0;
+    c->breakdown = 0;
+    c->first = 1;
+    c->converged = 0;
+    c->zero_x = 0;
+    c->hist_len = 0;
+    c->true_res = 0;
+    c->est = 0;
+    if (c->bnorm == 0.0) {          // krylov.py:73-75: x = 0, 0 iterations, converged
+      c->zero_x = 1;
+      mark_done(a, c, 1);
+    } else {
+      c->target = c->tol * sqrt(t1);
+      c->phase = PH_RESID;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Tick kernel 1: SpMV (inner w = s.(A q_k)) or residual (t = b - A x, r = s.t) + cycle decisions.
+// ------------------------------------------------------------------------------------------------
+template <int DIM>
+__global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
+  __shared__ double red[2][PT / 32];
+  __shared__ int sflag;
+  const int b = blockIdx.x / a.nsb, sb = blockIdx.x % a.nsb;
+  if (b >= a.nb) return;
+  ModeCtl* c = a.ctl + b;
+  const int phase = c->phase;
+  if (phase != PH_INNER && phase != PH_START && phase != PH_RESID) return;
+  const bool resid = phase == PH_RESID;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double om = c->omega;
+  const int k = c->k;
+  const double2* x = resid ? a.X + (size_t)b * a.ld : qvec(a, b, k);
+  const double xs = resid ? 1.0 : a.qs[b * a.jcap + k];
+  double2* out = resid ? qvec(a, b, 0) : a.W + (size_t)b * a.ld;
+  const double2* rhs = a.RHS + (size_t)b * a.ld;
+  double tt = 0, rr = 0;
+  const int tasks = a.kind == 0 ? a.op.nfree + a.op.npf : a.n;
+  const int t0 = (sb * (PT / 32) + warp) * SPMV_TPW;
+  for (int ti = 0; ti < SPMV_TPW; ++ti) {
+    const int task = t0 + ti;
+    if (task >= tasks) break;
+    if (a.kind == 0 && task < a.op.nfree) {
+      double2 acc[DIM];
+      saddle_vel_row<DIM>(a.op, task, om, x, lane, acc);
+      const double2 s = a.jacobi ? saddle_jacobi(a.op, task, om) : make_double2(1.0, 0.0);
+      if (lane < DIM) {
+        double2 v = acc[0];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
+        const int row = task * DIM + lane;
+        if (resid) {
+          const double2 t = csub(rhs[row], v);
+          const double2 r = cmul(s, t);
+          out[row] = r;
+          tt += cabs2(t);
+          rr += cabs2(r);
+        } else {
+          out[row] = cmul(s, cscale(v, xs));
+        }
+      }
+    } else {
+      const int row = a.kind == 0 ? a.op.nfv + (task - a.op.nfree) : task;
+      const double2 v = a.kind == 0 ? saddle_pres_row<DIM>(a.op, task - a.op.nfree, x, lane)
+                                    : csr_row(a.csr, a.csr.nvals > 1 ? b : 0, task, x, lane);
+      if (lane == 0) {
+        const double2 s = a.kind == 0 ? make_double2(1.0, 0.0) : row_scale<DIM>(a, b, row, om);
+        if (resid) {
+          const double2 t = csub(rhs[row], v);
+          const double2 r = cmul(s, t);
+          out[row] = r;
+          tt += cabs2(t);
+          rr += cabs2(r);
+        } else {
+          out[row] = cmul(s, cscale(v, xs));
+        }
+      }
+    }
+  }
+  if (resid) {
+    tt = warp_sum(tt);
+    rr = warp_sum(rr);
+    if (lane == 0) { red[0][warp] = tt; red[1][warp] = rr; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s0 = 0, s1 = 0;
+      for (int w = 0; w < PT / 32; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
+      a.spart[(size_t)b * a.nsb + sb] = make_double2(s0, s1);
+    }
+  }
+  if (!last_cta(a, b, 0, a.nsb, &sflag)) return;
+  if (!resid) {
+    if (threadIdx.x == 0 && phase == PH_START) c->phase = PH_INNER;
+    return;
+  }
+  // Residual reduction (fixed order) and the cycle-boundary decisions (krylov.py:93-103,155-162).
+  __shared__ double2 rsum[PT];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = threadIdx.x; q < a.nsb; q += PT) {
+    const double2 v = __ldcg(a.spart + (size_t)b * a.nsb + q);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  rsum[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = PT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) rsum[threadIdx.x] = cadd(rsum[threadIdx.x], rsum[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tn = sqrt(rsum[0].x), rn = sqrt(rsum[0].y);
+    bool done = false;
+    if (!c->first) {
+      c->true_res = tn / c->bnorm;
+      if (c->true_res <= c->tol) { mark_done(a, c, 1); done = true; }
+      else if (c->breakdown) { mark_done(a, c, 0); done = true; }
+      else if (c->gk_last <= c->target) c->target *= 0.25;
+    }
+    if (!done) {
+      if (c->iters >= c->maxiter) {
+        mark_done(a, c, 0);
+      } else if (rn == 0.0) {
+        mark_done(a, c, 1);
+      } else {
+        c->beta = rn;
+        c->k = 0;
+        c->breakdown = 0;
+        c->first = 0;
+        a.qs[b * a.jcap] = 1.0 / rn;
+        c->phase = PH_START;
+      }
+    }
+  }
+  __syncthreads();
+  if (c->phase == PH_START) {
+    double2* g = a.G + (size_t)b * a.jcap;
+    for (int j = threadIdx.x; j < a.jcap; j += PT) g[j] = make_double2(j == 0 ? c->beta : 0.0, 0.0);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Basis-streaming passes.  A CTA owns one fixed segment of rows of one mode and streams the
+// (J x rows) slab of raw basis vectors through shared memory in chunks (cp.async, 2 stages).
+// ------------------------------------------------------------------------------------------------
+enum PassKind : int { PASS_A = 1, PASS_B = 2, PASS_C = 3, PASS_X = 4 };
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int pow2floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ double2 coef[256];
+  __shared__ double2 red[PT];
+  __shared__ int sflag;
+  const int b = blockIdx.x / a.nseg, s = blockIdx.x % a.nseg;
+  if (b >= a.nb) return;
+  ModeCtl* c = a.ctl + b;
+  const int phase = c->phase;
+  if (PASS == PASS_X ? phase != PH_XUPDATE : phase != PH_INNER) return;
+  const int k = c->k;
+  const int J = PASS == PASS_X ? k : k + 1;
+  const int tid = threadIdx.x;
+  double* qs = a.qs + (size_t)b * a.jcap;
+  // coefficients of the update (qs folded in): B: qs_j c_j, C: qs_j c2_j, X: y_j (already scaled)
+  if (PASS == PASS_B || PASS == PASS_C) {
+    const double2* cc = (PASS == PASS_B ? a.C1 : a.C2) + (size_t)b * a.jcap;
+    for (int j = tid; j < J; j += PT) coef[j] = cscale(cc[j], qs[j]);
+  } else if (PASS == PASS_X) {
+    for (int j = tid; j < J; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
+  }
+  const int Tj = J > 0 ? max(1, pow2floor(PT / J)) : 1;
+  int m = (a.cap - J * Tj) / (32 * (J + 1));
+  m = max(1, min(m, a.seg_rows / 32));
+  const int R = 32 * m;
+  const int stride = R + Tj;
+  const int stage_elems = J * stride + R;
+  double2* stage[2] = {smem, smem + a.cap};
+  const int64_t row_begin = (int64_t)s * a.seg_rows;
+  const int64_t row_end = min(row_begin + a.seg_rows, a.ld);
+  const int nchunks = (int)((row_end - row_begin + R - 1) / R);
+  double2* vec = (PASS == PASS_X ? a.X : a.W) + (size_t)b * a.ld;
+  const double2* Qb = a.Q + (size_t)b * a.jcap * a.ld;
+
+  auto load_chunk = [&](int ci, double2* st) {
+    const int64_t r0 = row_begin + (int64_t)ci * R;
+    const int rows = (int)min((int64_t)R, row_end - r0);
+    const int total = J * rows;
+    for (int idx = tid; idx < total; idx += PT) {
+      const int j = idx / rows, r = idx - j * rows;
+      cp16(st + j * stride + r, Qb + (size_t)j * a.ld + r0 + r);
+    }
+    for (int r = tid; r < rows; r += PT) cp16(st + J * stride + r, vec + r0 + r);
+    cp_commit();
+  };
+
+  double2 dot = make_double2(0.0, 0.0);   // phase-2 accumulator of thread (j = tid/Tj, sub = tid%Tj)
+  double nrm = 0.0;                        // pass C: ||w||^2 of rows this thread finalises
+  const int my_j = tid / Tj, my_sub = tid % Tj;
+  if (J > 0) load_chunk(0, stage[0]);
+  __syncthreads();
+  for (int ci = 0; ci < nchunks; ++ci) {
+    double2* st = stage[ci & 1];
+    if (ci + 1 < nchunks) {
+      load_chunk(ci + 1, stage[(ci + 1) & 1]);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int64_t r0 = row_begin + (int64_t)ci * R;
+    const int rows = (int)min((int64_t)R, row_end - r0);
+    double2* V = st + J * stride;
+    if (PASS != PASS_A) {
+      // phase 1: V[r] (+/-)= sum_j S[j][r] coef[j]
+      if (rows >= PT) {
+        for (int r = tid; r < rows; r += PT) {
+          double2 acc = make_double2(0.0, 0.0);
+          for (int j = 0; j < J; ++j) {
+            const double2 q = st[j * stride + r], cf = coef[j];
+            acc.x += q.x * cf.x - q.y * cf.y;
+            acc.y += q.x * cf.y + q.y * cf.x;
+          }
+          const double2 v = PASS == PASS_X ? cadd(V[r], acc) : csub(V[r], acc);
+          V[r] = v;
+          if (PASS == PASS_C) nrm += cabs2(v);
+        }
+      } else {
+        const int JS = PT / rows;
+        const int r = tid % rows, js = tid / rows;
+        if (js < JS) {
+          double2 acc = make_double2(0.0, 0.0);
+          for (int j = js; j < J; j += JS) {
+            const double2 q = st[j * stride + r], cf = coef[j];
+            acc.x += q.x * cf.x - q.y * cf.y;
+            acc.y += q.x * cf.y + q.y * cf.x;
+          }
+          red[js * rows + r] = acc;
+        }
+        __syncthreads();
+        if (tid < rows) {
+          double2 acc = red[tid];
+          for (int q = 1; q < JS; ++q) acc = cadd(acc, red[q * rows + tid]);
+          const double2 v = PASS == PASS_X ? cadd(V[tid], acc) : csub(V[tid], acc);
+          V[tid] = v;
+          if (PASS == PASS_C) nrm += cabs2(v);
+        }
+      }
+      __syncthreads();
+      // write back the updated vector (w for B, Q[k+1] raw for C, x for X)
+      double2* dst = PASS == PASS_C ? qvec(a, b, k + 1) : vec;
+      for (int r = tid; r < rows; r += PT) dst[r0 + r] = V[r];
+    }
+    if (PASS == PASS_A || PASS == PASS_B) {
+      // phase 2: dot[j] += sum_r conj(S[j][r]) V[r]
+      if (my_j < J) {
+        for (int r = my_sub; r < rows; r += Tj) {
+          const double2 q = st[my_j * stride + r], v = V[r];
+          dot.x += q.x * v.x + q.y * v.y;
+          dot.y += q.x * v.y - q.y * v.x;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && row_begin < a.n) {
+    // algorithmic bytes of this CTA: J basis rows read + vector read (+ vector/basis row written)
+    const int64_t real_rows = min(row_end, (int64_t)a.n) - row_begin;
+    atomicAdd(a.bytes + PASS, (unsigned long long)((J + (PASS == PASS_A ? 1 : 2)) * real_rows * 16));
+  }
+  if (PASS == PASS_X) {
+    if (!last_cta(a, b, PASS, a.nseg, &sflag)) return;
+    if (tid == 0) c->phase = PH_RESID;
+    return;
+  }
+  // per-CTA partials
+  double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
+  if (PASS == PASS_C) {
+    red[tid] = make_double2(nrm, 0.0);
+    __syncthreads();
+    for (int o = PT / 2; o > 0; o >>= 1) {
+      if (tid < o) red[tid].x += red[tid + o].x;
+      __syncthreads();
+    }
+    if (tid == 0) part[0] = red[0];
+  } else {
+    red[tid] = dot;
+    __syncthreads();
+    if (tid < J) {
+      double2 acc = red[tid * Tj];
+      for (int q = 1; q < Tj; ++q) acc = cadd(acc, red[tid * Tj + q]);
+      part[tid] = acc;
+    }
+  }
+  if (!last_cta(a, b, PASS, a.nseg, &sflag)) return;
+
+  // ---- last CTA of this mode: reduce partials over segments in fixed order ----
+  const double2* pb = a.part + (size_t)b * a.nseg * a.jcap;
+  const int JR = PASS == PASS_C ? 1 : J;
+  const int SL = max(1, PT / JR);      // slices over segments
+  {
+    const int j = tid % JR, sl = tid / JR;
+    double2 acc = make_double2(0.0, 0.0);
+    if (sl < SL)
+      for (int q = sl; q < a.nseg; q += SL) acc = cadd(acc, __ldcg(pb + (size_t)q * a.jcap + j));
+    red[tid] = acc;
+  }
+  __syncthreads();
+  if (PASS == PASS_A || PASS == PASS_B) {
+    double2* out = (PASS == PASS_A ? a.C1 : a.C2) + (size_t)b * a.jcap;
+    if (tid < JR) {
+      double2 acc = red[tid];
+      for (int q = 1; q < SL; ++q) acc = cadd(acc, red[q * JR + tid]);
+      out[tid] = cscale(acc, qs[tid]);
+    }
+    return;
+  }
+  // PASS_C: Givens update (krylov.py:115-149), single thread for the serial recurrence.
+  __shared__ double2 y[256];
+  __shared__ int s_solve;
+  if (tid == 0) {
+    double nsq = 0;
+    for (int q = 0; q < SL; ++q) nsq += red[q].x;
+    const double hk = sqrt(nsq);
+    const int jc = a.jcap;
+    double2* h = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
+    const double2* c1 = a.C1 + (size_t)b * jc;
+    const double2* c2 = a.C2 + (size_t)b * jc;
+    for (int i = 0; i <= k; ++i) h[i] = cadd(c1[i], c2[i]);
+    double2* cs = a.CS + (size_t)b * a.restart;
+    double2* sn = a.SN + (size_t)b * a.restart;
+    double2* g = a.G + (size_t)b * jc;
+    for (int i = 0; i < k; ++i) {
+      const double2 hi = h[i], hi1 = h[i + 1];
+      const double2 tmp = cadd(cmul(cs[i], hi), cmul(sn[i], hi1));
+      h[i + 1] = cadd(cmul(make_double2(-sn[i].x, sn[i].y), hi), cmul(conjd(cs[i]), hi1));
+      h[i] = tmp;
+    }
+    const double ahkk = hypot(h[k].x, h[k].y);
+    const double denom = sqrt(ahkk * ahkk + hk * hk);
+    int exit_cycle = 0;
+    if (denom == 0.0) {                       // krylov.py:124-129
+      c->breakdown = 1;
+      c->iters += 1;
+      exit_cycle = 1;
+    } else {
+      const double2 csk = cscale(conjd(h[k]), 1.0 / denom);
+      const double2 snk = make_double2(hk / denom, 0.0);
+      cs[k] = csk;
+      sn[k] = snk;
+      h[k] = cadd(cmul(csk, h[k]), cscale(snk, hk));
+      h[k + 1] = make_double2(0.0, 0.0);
+      const double2 gk = g[k];
+      g[k + 1] = cmul(make_double2(-snk.x, snk.y), gk);
+      g[k] = cmul(csk, gk);
+      c->iters += 1;
+      const double est = hypot(g[k + 1].x, g[k + 1].y);
+      c->est = est;
+      if (c->hist_len < a.hist_cap) a.hist[(size_t)b * a.hist_cap + c->hist_len] = est;
+      c->hist_len += 1;
+      if (hk <= 1e-14 * fabs(c->beta)) {      // happy breakdown (krylov.py:141-145)
+        c->breakdown = 1;
+        c->k = k + 1;
+        exit_cycle = 1;
+      } else {
+        qs[k + 1] = 1.0 / hk;
+        c->k = k + 1;
+        if (est <= c->target || c->k >= a.restart || c->iters >= c->maxiter) exit_cycle = 1;
+      }
+    }
+    s_solve = 0;
+    if (exit_cycle) {
+      const int kk = c->k;
+      c->gk_last = hypot(g[kk].x, g[kk].y);
+      if (kk > 0) {
+        s_solve = kk;
+      } else {
+        c->phase = PH_RESID;
+      }
+    }
+  }
+  __syncthreads();
+  const int kk = s_solve;
+  if (kk == 0) return;
+  // Cycle end: y = H[:k,:k]^-1 g[:k] (column-oriented back substitution, krylov.py:151-153,167-168)
+  const int jc = a.jcap;
+  const double2* hb = a.H + (size_t)b * a.restart * jc;
+  const double2* g = a.G + (size_t)b * jc;
+  for (int i = tid; i < kk; i += PT) y[i] = g[i];
+  __syncthreads();
+  for (int j = kk - 1; j >= 0; --j) {
+    if (tid == 0) y[j] = cdiv(y[j], hb[(size_t)j * jc + j]);
+    __syncthreads();
+    const double2 yj = y[j];
+    for (int i = tid; i < j; i += PT) y[i] = csub(y[i], cmul(hb[(size_t)j * jc + i], yj));
+    __syncthreads();
+  }
+  for (int i = tid; i < kk; i += PT) a.Y[(size_t)b * jc + i] = cscale(y[i], qs[i]);
+  __syncthreads();
+  if (tid == 0) c->phase = PH_XUPDATE;
+}
+
+__global__ void k_finalize(KArgs a) {
+  const int b = blockIdx.y;
+  if (b >= a.nb || !a.ctl[b].zero_x) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ld; i += (int64_t)gridDim.x * blockDim.x)
+    a.X[(size_t)b * a.ld + i] = make_double2(0.0, 0.0);
+}
+
+// Jacobi scale of a generic CSR matrix: 1/diag, 1 where the diagonal is zero or absent (krylov.py:49-60).
+__global__ void k_csr_jacobi(SsCsrDev A, double2* __restrict__ out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int set = blockIdx.y;
+  if (row >= A.n) return;
+  double2 d = make_double2(0.0, 0.0);
+  for (int e = A.indptr[row]; e < A.indptr[row + 1]; ++e)
+    if (A.indices[e] == row) d = cadd(d, A.vals[(size_t)set * A.nnz + e]);
+  out[(size_t)set * A.n + row] = (d.x == 0.0 && d.y == 0.0) ? make_double2(1.0, 0.0) : cdiv(make_double2(1.0, 0.0), d);
+}
+
+// True residual partials: spart[b][blk] = (||b - A x||^2, ||b||^2) over the block's rows
+// (ComplexSaddleSystem.residual_norm, assembly.py:357-362; gmres_solve, krylov.py:203-207).
+template <int DIM>
+__global__ void __launch_bounds__(PT) k_true_resid(KArgs a) {
+  __shared__ double red[2][PT / 32];
+  const int b = blockIdx.x / a.nsb, sb = blockIdx.x % a.nsb;
+  if (b >= a.nb) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double om = a.ctl[b].omega;
+  const double2* x = a.X + (size_t)b * a.ld;
+  const double2* rhs = a.RHS + (size_t)b * a.ld;
+  double tt = 0, bb = 0;
+  const int tasks = a.kind == 0 ? a.op.nfree + a.op.npf : a.n;
+  const int t0 = (sb * (PT / 32) + warp) * SPMV_TPW;
+  for (int ti = 0; ti < SPMV_TPW; ++ti) {
+    const int task = t0 + ti;
+    if (task >= tasks) break;
+    if (a.kind == 0 && task < a.op.nfree) {
+      double2 acc[DIM];
+      saddle_vel_row<DIM>(a.op, task, om, x, lane, acc);
+      if (lane < DIM) {
+        double2 v = acc[0];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
+        const double2 rb = rhs[task * DIM + lane];
+        tt += cabs2(csub(rb, v));
+        bb += cabs2(rb);
+      }
+    } else {
+      const int row = a.kind == 0 ? a.op.nfv + (task - a.op.nfree) : task;
+      const double2 v = a.kind == 0 ? saddle_pres_row<DIM>(a.op, task - a.op.nfree, x, lane)
+                                    : csr_row(a.csr, a.csr.nvals > 1 ? b : 0, task, x, lane);
+      if (lane == 0) {
+        const double2 rb = rhs[row];
+        tt += cabs2(csub(rb, v));
+        bb += cabs2(rb);
+      }
+    }
+  }
+  tt = warp_sum(tt);
+  bb = warp_sum(bb);
+  if (lane == 0) { red[0][warp] = tt; red[1][warp] = bb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0, s1 = 0;
+    for (int w = 0; w < PT / 32; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
+    a.spart[(size_t)b * a.nsb + sb] = make_double2(s0, s1);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Host side
+// ------------------------------------------------------------------------------------------------
+struct ss_krylov {
+  int device = 0;
+  KArgs a{};
+  int max_batch = 0;
+  std::vector<void*> allocs;
+  cudaStream_t cap_stream = nullptr;
+  std::map<int64_t, cudaGraphExec_t> graphs;
+  int* h_done = nullptr;       // pinned
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int ticks_per_graph = 8;
+  size_t smem_pass = 0;
+  int64_t last_ticks = 0;
+  int64_t last_launches = 0;
+  double2* csr_vals_owned = nullptr;
+};
+
+template <class T>
+static int kalloc(ss_krylov* K, size_t count, T** p) {
+  SS_CUDA(cudaMalloc((void**)p, std::max<size_t>(1, count) * sizeof(T)));
+  K->allocs.push_back((void*)*p);
+  SS_CUDA(cudaMemset(*p, 0, std::max<size_t>(1, count) * sizeof(T)));
+  return SS_OK;
+}
+
+static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, int64_t hist_cap) {
+  if (restart < 1 || restart > 240) { ss_set_error("restart must lie in [1, 240]"); return SS_ERR_ARG; }
+  if (max_batch < 1) { ss_set_error("max_batch must be >= 1"); return SS_ERR_ARG; }
+  KArgs& a = K->a;
+  a.n = n;
+  a.ld = ss_round_up(std::max(n, 1), 32);
+  a.restart = restart;
+  a.jcap = restart + 1;
+  a.hist_cap = std::max<int64_t>(1, hist_cap);
+  // segment rows depend on n only (batch-composition invariance of every reduction)
+  int64_t seg = ss_round_up((a.ld + 63) / 64, 32);
+  seg = std::min<int64_t>(4096, std::max<int64_t>(256, seg));
+  a.seg_rows = (int)seg;
+  a.nseg = (int)((a.ld + seg - 1) / seg);
+  a.cap = 32 * a.jcap + 288;
+  K->max_batch = max_batch;
+  const size_t B = max_batch;
+  int rc;
+  if ((rc = kalloc(K, B * a.jcap * a.ld, &a.Q))) return rc;
+  if ((rc = kalloc(K, B * a.ld, &a.W))) return rc;
+  if ((rc = kalloc(K, B * a.ld, &a.X))) return rc;
+  if ((rc = kalloc(K, B * a.ld, &a.RHS))) return rc;
+  if ((rc = kalloc(K, B * a.jcap, &a.qs))) return rc;
+  if ((rc = kalloc(K, B * restart * a.jcap, &a.H))) return rc;
+  if ((rc = kalloc(K, B * a.jcap, &a.G))) return rc;
+  if ((rc = kalloc(K, B * restart, &a.CS))) return rc;
+  if ((rc = kalloc(K, B * restart, &a.SN))) return rc;
+  if ((rc = kalloc(K, B * a.jcap, &a.C1))) return rc;
+  if ((rc = kalloc(K, B * a.jcap, &a.C2))) return rc;
+  if ((rc = kalloc(K, B * a.jcap, &a.Y))) return rc;
+  if ((rc = kalloc(K, B * a.nseg * a.jcap, &a.part))) return rc;
+  if ((rc = kalloc(K, B * 8, &a.counters))) return rc;
+  if ((rc = kalloc(K, 1, &a.n_done))) return rc;
+  if ((rc = kalloc(K, B, &a.ctl))) return rc;
+  if ((rc = kalloc(K, B * a.hist_cap, &a.hist))) return rc;
+  if ((rc = kalloc(K, 8, &a.bytes))) return rc;
+  SS_CUDA(cudaHostAlloc((void**)&K->h_done, 2 * sizeof(int), cudaHostAllocDefault));
+  SS_CUDA(cudaStreamCreateWithFlags(&K->cap_stream, cudaStreamNonBlocking));
+  SS_CUDA(cudaEventCreateWithFlags(&K->ev[0], cudaEventDisableTiming));
+  SS_CUDA(cudaEventCreateWithFlags(&K->ev[1], cudaEventDisableTiming));
+  K->smem_pass = (size_t)2 * a.cap * sizeof(double2);
+  if (K->smem_pass + 3 * 256 * sizeof(double2) + 64 > 227 * 1024) {
+    ss_set_error("restart too large for the shared-memory staging of the basis passes");
+    return SS_ERR_ARG;
+  }
+  auto setattr = [&](const void* f) { return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K->smem_pass); };
+  SS_CUDA(setattr((const void*)k_pass<PASS_A>));
+  SS_CUDA(setattr((const void*)k_pass<PASS_B>));
+  SS_CUDA(setattr((const void*)k_pass<PASS_C>));
+  SS_CUDA(setattr((const void*)k_pass<PASS_X>));
+  K->ticks_per_graph = n < 200000 ? 16 : 2;
+  return SS_OK;
+}
+
+extern "C" int ss_krylov_create_saddle(const ss_pattern* P, int max_batch, int restart, int64_t hist_cap,
+                                       ss_krylov** out) {
+  if (!P || !out) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  SS_CUDA(cudaSetDevice(P->device));
+  ss_krylov* K = new ss_krylov();
+  K->device = P->device;
+  K->a.kind = 0;
+  K->a.op = P->op;
+  const int tasks = P->nfree + P->npf;
+  K->a.nsb = (tasks + (PT / 32) * SPMV_TPW - 1) / ((PT / 32) * SPMV_TPW);
+  int rc = krylov_common_init(K, P->op.n, max_batch, restart, hist_cap);
+  if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
+  if (rc) { delete K; return rc; }
+  *out = K;
+  return SS_OK;
+}
+
+// Generic CSR operator: values for nvals sets (1 = shared); scale (optional) per set.
+extern "C" int ss_krylov_create_csr(int device, int n, int64_t nnz, const int32_t* indptr, const int32_t* indices,
+                                    int nvals, const double* vals, const double* scale, int jacobi_from_diag,
+                                    int max_batch, int restart, int64_t hist_cap, ss_krylov** out) {
+  if (!out || n <= 0 || !indptr || (nnz > 0 && (!indices || !vals)) || nvals < 1) {
+    ss_set_error("bad arguments");
+    return SS_ERR_ARG;
+  }
+  SS_CUDA(cudaSetDevice(device));
+  ss_krylov* K = new ss_krylov();
+  K->device = device;
+  K->a.kind = 1;
+  SsCsrDev& A = K->a.csr;
+  A.n = n;
+  A.nnz = nnz;
+  A.nvals = nvals;
+  int rc = SS_OK;
+  int *ip, *ix;
+  double2 *v, *sc = nullptr;
+  if (!rc) rc = kalloc(K, (size_t)n + 1, &ip);
+  if (!rc) rc = kalloc(K, (size_t)nnz, &ix);
+  if (!rc) rc = kalloc(K, (size_t)nvals * nnz, &v);
+  if (!rc && (scale || jacobi_from_diag)) rc = kalloc(K, (size_t)nvals * n, &sc);
+  if (rc) { delete K; return rc; }
+  SS_CUDA(cudaMemcpy(ip, indptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+  if (nnz) SS_CUDA(cudaMemcpy(ix, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+  if (nnz) SS_CUDA(cudaMemcpy(v, vals, sizeof(double2) * nvals * nnz, cudaMemcpyHostToDevice));
+  if (scale) SS_CUDA(cudaMemcpy(sc, scale, sizeof(double2) * nvals * n, cudaMemcpyHostToDevice));
+  A.indptr = ip; A.indices = ix; A.vals = v; A.scale = sc;
+  if (jacobi_from_diag && !scale) {
+    k_csr_jacobi<<<dim3((n + 255) / 256, nvals), 256>>>(A, sc);
+    ss_count_launch();
+    SS_CUDA(cudaGetLastError());
+  }
+  K->a.nsb = (n + (PT / 32) * SPMV_TPW - 1) / ((PT / 32) * SPMV_TPW);
+  rc = krylov_common_init(K, n, max_batch, restart, hist_cap);
+  if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
+  if (rc) { delete K; return rc; }
+  *out = K;
+  return SS_OK;
+}
+
+extern "C" void ss_krylov_destroy(ss_krylov* K) {
+  if (!K) return;
+  cudaSetDevice(K->device);
+  for (auto& kv : K->graphs) cudaGraphExecDestroy(kv.second);
+  for (void* p : K->allocs) cudaFree(p);
+  if (K->h_done) cudaFreeHost(K->h_done);
+  if (K->cap_stream) cudaStreamDestroy(K->cap_stream);
+  for (auto e : K->ev) if (e) cudaEventDestroy(e);
+  delete K;
+}
+
+// info: [n, ld, restart, nseg, seg_rows, nsb, max_batch, ticks_per_graph, smem_pass, kind]
+extern "C" int ss_krylov_info(const ss_krylov* K, int64_t* info) {
+  if (!K || !info) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  info[0] = K->a.n; info[1] = K->a.ld; info[2] = K->a.restart; info[3] = K->a.nseg; info[4] = K->a.seg_rows;
+  info[5] = K->a.nsb; info[6] = K->max_batch; info[7] = K->ticks_per_graph; info[8] = (int64_t)K->smem_pass;
+  info[9] = K->a.kind;
+  return SS_OK;
+}
+
+extern "C" int ss_krylov_buffers(ss_krylov* K, double** rhs, double** x, int64_t* ld) {
+  if (!K) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  if (rhs) *rhs = (double*)K->a.RHS;
+  if (x) *x = (double*)K->a.X;
+  if (ld) *ld = K->a.ld;
+  return SS_OK;
+}
+
+template <int DIM>
+static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
+  const unsigned gs = (unsigned)(a.nb * a.nseg);
+  k_tick_spmv<DIM><<<a.nb * a.nsb, PT, 0, st>>>(a);
+  SS_LAUNCH_CHECK();
+  k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+  SS_LAUNCH_CHECK();
+  k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+  SS_LAUNCH_CHECK();
+  k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
+  SS_LAUNCH_CHECK();
+  k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+static int tick_dim(const ss_krylov* K) { return K->a.kind == 0 ? K->a.op.dim : 2; }
+
+static int get_graph(ss_krylov* K, int nb, int jacobi, cudaGraphExec_t* out) {
+  const int64_t key = (int64_t)nb * 4 + jacobi * 2;
+  auto it = K->graphs.find(key);
+  if (it != K->graphs.end()) { *out = it->second; return SS_OK; }
+  KArgs a = K->a;
+  a.nb = nb;
+  a.jacobi = jacobi;
+  cudaGraph_t g;
+  SS_CUDA(cudaStreamBeginCapture(K->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = SS_OK;
+  for (int t = 0; t < K->ticks_per_graph && !rc; ++t)
+    rc = tick_dim(K) == 3 ? launch_tick<3>(K, a, K->cap_stream) : launch_tick<2>(K, a, K->cap_stream);
+  cudaError_t e = cudaStreamEndCapture(K->cap_stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) { ss_set_error(std::string("graph capture failed: ") + cudaGetErrorString(e)); return SS_ERR_CUDA; }
+  cudaGraphExec_t ex;
+  SS_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  K->graphs[key] = ex;
+  *out = ex;
+  return SS_OK;
+}
+
+// Solve nb modes.  rhs/x0 are read from the engine's own RHS/X buffers (see ss_krylov_buffers)
+// when rhs_dev / x_dev are null, otherwise copied in (device pointers, leading dimension ld_in).
+// On return X holds the solutions (also copied to x_dev when given).
+// out_int[b*6 + {0: iterations, 1: converged flag, 2: breakdown, 3: phase, 4: history length, 5: zero rhs}]
+// out_dbl[b*4 + {0: true residual at last cycle end, 1: last estimate, 2: ||b||, 3: target}]
+extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, const int* sets_host,
+                               const double* rhs_dev, double* x_dev, int64_t ld_in, int use_x0, double tol,
+                               int64_t maxiter, int jacobi, void* stream_, int64_t* out_int, double* out_dbl) {
+  if (!K || nb < 1 || nb > K->max_batch || !omegas_host) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  if (!(tol > 0.0 && tol < 1.0)) { ss_set_error("tolerance must lie in (0, 1)"); return SS_ERR_ARG; }
+  if (maxiter < 0 || maxiter > INT32_MAX) { ss_set_error("bad maxiter"); return SS_ERR_ARG; }
+  SS_CUDA(cudaSetDevice(K->device));
+  cudaStream_t st = (cudaStream_t)stream_;
+  KArgs a = K->a;
+  a.nb = nb;
+  a.jacobi = jacobi;
+  const int64_t launches0 = ss_launch_counter();
+  std::vector<ModeCtl> ctl(nb);
+  for (int b = 0; b < nb; ++b) {
+    ModeCtl c{};
+    c.phase = PH_IDLE;
+    c.maxiter = (int)maxiter;
+    c.restart = a.restart;
+    c.tol = tol;
+    c.omega = omegas_host[b];
+    c.set = sets_host ? sets_host[b] : b;
+    ctl[b] = c;
+  }
+  SS_CUDA(cudaMemcpyAsync(a.ctl, ctl.data(), sizeof(ModeCtl) * nb, cudaMemcpyHostToDevice, st));
+  SS_CUDA(cudaMemsetAsync(a.n_done, 0, sizeof(int), st));
+  if (rhs_dev)
+    SS_CUDA(cudaMemcpy2DAsync(a.RHS, a.ld * sizeof(double2), rhs_dev, ld_in * sizeof(double2), a.n * sizeof(double2),
+                              nb, cudaMemcpyDeviceToDevice, st));
+  if (use_x0 && x_dev)
+    SS_CUDA(cudaMemcpy2DAsync(a.X, a.ld * sizeof(double2), x_dev, ld_in * sizeof(double2), a.n * sizeof(double2), nb,
+                              cudaMemcpyDeviceToDevice, st));
+  else if (!use_x0)
+    SS_CUDA(cudaMemsetAsync(a.X, 0, sizeof(double2) * a.ld * nb, st));
+  if (tick_dim(K) == 3) k_init<3><<<nb * a.nseg, PT, 0, st>>>(a);
+  else k_init<2><<<nb * a.nseg, PT, 0, st>>>(a);
+  SS_LAUNCH_CHECK();
+  cudaGraphExec_t g;
+  int rc = get_graph(K, nb, jacobi, &g);
+  if (rc) return rc;
+  const int per_graph_launches = 5 * K->ticks_per_graph;
+  // tick bound: every mode finishes within maxiter inner ticks + 2 ticks per cycle
+  const int64_t max_ticks = maxiter + 3 * (maxiter / std::max<int64_t>(1, std::min<int64_t>(a.restart, maxiter + 1)) + 2) + 16;
+  int64_t ticks = 0;
+  int it = 0;
+  bool finished = false;
+  while (!finished) {
+    SS_CUDA(cudaGraphLaunch(g, st));
+    ss_count_launch(per_graph_launches);
+    ticks += K->ticks_per_graph;
+    SS_CUDA(cudaMemcpyAsync(K->h_done + (it & 1), a.n_done, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaEventRecord(K->ev[it & 1], st));
+    if (it > 0) {
+      SS_CUDA(cudaEventSynchronize(K->ev[(it - 1) & 1]));
+      if (K->h_done[(it - 1) & 1] >= nb) finished = true;
+    }
+    if (ticks > max_ticks + 4 * K->ticks_per_graph) {
+      ss_set_error("GMRES tick bound exceeded (internal state machine error)");
+      return SS_ERR_STATE;
+    }
+    ++it;
+  }
+  SS_CUDA(cudaEventSynchronize(K->ev[(it - 1) & 1]));
+  k_finalize<<<dim3(64, nb), 256, 0, st>>>(a);
+  SS_LAUNCH_CHECK();
+  if (x_dev)
+    SS_CUDA(cudaMemcpy2DAsync(x_dev, ld_in * sizeof(double2), a.X, a.ld * sizeof(double2), a.n * sizeof(double2), nb,
+                              cudaMemcpyDeviceToDevice, st));
+  SS_CUDA(cudaMemcpyAsync(ctl.data(), a.ctl, sizeof(ModeCtl) * nb, cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  K->last_ticks = ticks;
+  K->last_launches = ss_launch_counter() - launches0;
+  for (int b = 0; b < nb; ++b) {
+    if (out_int) {
+      out_int[b * 6 + 0] = ctl[b].iters;
+      out_int[b * 6 + 1] = ctl[b].converged;
+      out_int[b * 6 + 2] = ctl[b].breakdown;
+      out_int[b * 6 + 3] = ctl[b].phase;
+      out_int[b * 6 + 4] = ctl[b].hist_len;
+      out_int[b * 6 + 5] = ctl[b].zero_x;
+    }
+    if (out_dbl) {
+      out_dbl[b * 4 + 0] = ctl[b].true_res;
+      out_dbl[b * 4 + 1] = ctl[b].est;
+      out_dbl[b * 4 + 2] = ctl[b].bnorm;
+      out_dbl[b * 4 + 3] = ctl[b].target;
+    }
+  }
+  return SS_OK;
+}
+
+extern "C" int ss_krylov_last_stats(const ss_krylov* K, int64_t* ticks, int64_t* launches) {
+  if (!K) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  if (ticks) *ticks = K->last_ticks;
+  if (launches) *launches = K->last_launches;
+  return SS_OK;
+}
+
+extern "C" int ss_krylov_history(const ss_krylov* K, int mode, int64_t count, double* out) {
+  if (!K || !out || mode < 0 || mode >= K->max_batch) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  count = std::min(count, K->a.hist_cap);
+  if (count > 0)
+    SS_CUDA(cudaMemcpy(out, K->a.hist + (size_t)mode * K->a.hist_cap, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  return SS_OK;
+}
+
+// One isolated basis pass (bench / profiling): runs k_pass<PASS_B> for nb modes, all forced into
+// phase INNER at basis index k (J = k+1 vectors).  Returns algorithmic bytes in *bytes.
+__global__ void k_force_inner(KArgs a, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.nb) return;
+  a.ctl[b].phase = PH_INNER;
+  a.ctl[b].k = k;
+  for (int j = 0; j <= k; ++j) a.qs[b * a.jcap + j] = 1.0;
+}
+
+extern "C" int ss_krylov_bench_pass(ss_krylov* K, int nb, int k, int which, int reps, void* stream_, float* ms,
+                                    int64_t* bytes) {
+  if (!K || nb < 1 || nb > K->max_batch || k < 0 || k >= K->a.restart) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  KArgs a = K->a;
+  a.nb = nb;
+  k_force_inner<<<(nb + 127) / 128, 128, 0, st>>>(a, k);
+  SS_LAUNCH_CHECK();
+  cudaEvent_t e0, e1;
+  SS_CUDA(cudaEventCreate(&e0));
+  SS_CUDA(cudaEventCreate(&e1));
+  const unsigned gs = (unsigned)(nb * a.nseg);
+  // warm-up
+  if (which == PASS_A) k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+  else k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+  SS_LAUNCH_CHECK();
+  SS_CUDA(cudaEventRecord(e0, st));
+  for (int r = 0; r < reps; ++r) {
+    if (which == PASS_A) k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+    else k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+  }
+  SS_CUDA(cudaEventRecord(e1, st));
+  SS_CUDA(cudaEventSynchronize(e1));
+  SS_CUDA(cudaEventElapsedTime(ms, e0, e1));
+  *ms /= reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const int64_t J = k + 1;
+  // A: read Q (J vectors) + w;  B: read Q + w, write w
+  *bytes = (int64_t)nb * 16 * a.n * (J + (which == PASS_A ? 1 : 2));
+  return SS_OK;
+}
+
+// True relative residuals ||b - A x|| / ||b|| (||A x|| when b = 0) of the workspace's X for nb modes.
+extern "C" int ss_krylov_residuals(ss_krylov* K, int nb, void* stream_, double* out_host) {
+  if (!K || nb < 1 || nb > K->max_batch || !out_host) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  KArgs a = K->a;
+  a.nb = nb;
+  if (K->a.kind == 0 && K->a.op.dim == 3) k_true_resid<3><<<nb * a.nsb, PT, 0, st>>>(a);
+  else k_true_resid<2><<<nb * a.nsb, PT, 0, st>>>(a);
+  SS_LAUNCH_CHECK();
+  std::vector<double2> h((size_t)nb * a.nsb);
+  SS_CUDA(cudaMemcpyAsync(h.data(), a.spart, sizeof(double2) * h.size(), cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < nb; ++b) {
+    double tt = 0, bb = 0;
+    for (int q = 0; q < a.nsb; ++q) { tt += h[(size_t)b * a.nsb + q].x; bb += h[(size_t)b * a.nsb + q].y; }
+    out_host[b] = bb == 0.0 ? std::sqrt(tt) : std::sqrt(tt) / std::sqrt(bb);
+  }
+  return SS_OK;
+}
+
+// Copy nb rows between caller device buffers and the workspace (dir 0: caller -> RHS, 1: caller -> X,
+// 2: X -> caller).
+extern "C" int ss_krylov_copy(ss_krylov* K, int nb, int dir, double* buf_dev, int64_t ld_in, void* stream_) {
+  if (!K || nb < 1 || nb > K->max_batch || !buf_dev) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  const KArgs& a = K->a;
+  const size_t w = (size_t)a.n * sizeof(double2);
+  if (dir == 0)
+    SS_CUDA(cudaMemcpy2DAsync(a.RHS, a.ld * 16, buf_dev, ld_in * 16, w, nb, cudaMemcpyDeviceToDevice, st));
+  else if (dir == 1)
+    SS_CUDA(cudaMemcpy2DAsync(a.X, a.ld * 16, buf_dev, ld_in * 16, w, nb, cudaMemcpyDeviceToDevice, st));
+  else
+    SS_CUDA(cudaMemcpy2DAsync(buf_dev, ld_in * 16, a.X, a.ld * 16, w, nb, cudaMemcpyDeviceToDevice, st));
+  return SS_OK;
+}
+
+// Jacobi scale of the CSR operator's value set `set` (jacobi_precondition on a matrix).
+extern "C" int ss_krylov_csr_scale(const ss_krylov* K, int set, double* out_host) {
+  if (!K || K->a.kind != 1 || !K->a.csr.scale || !out_host) { ss_set_error("no CSR scale"); return SS_ERR_ARG; }
+  SS_CUDA(cudaMemcpy(out_host, K->a.csr.scale + (size_t)set * K->a.csr.n, sizeof(double2) * K->a.csr.n,
+                     cudaMemcpyDeviceToHost));
+  return SS_OK;
+}
+
+// Instrumented solve for the roofline: identical kernels launched one by one (no graph) with
+// CUDA events on the launching stream between them; accumulates per-kernel-kind device time and
+// the algorithmic bytes each kind moved.  kind: 0 spmv, 1 passA, 2 passB, 3 passC, 4 passX.
+// ms_out[5], bytes_out[5], launches_out[5].
+template <int DIM>
+static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t max_ticks, double* ms_out,
+                         int64_t* launches_out) {
+  const unsigned gs = (unsigned)(a.nb * a.nseg);
+  cudaEvent_t ev[6];
+  for (auto& e : ev) SS_CUDA(cudaEventCreate(&e));
+  int64_t tick = 0;
+  int done = 0;
+  while (tick < max_ticks) {
+    SS_CUDA(cudaEventRecord(ev[0], st));
+    k_tick_spmv<DIM><<<a.nb * a.nsb, PT, 0, st>>>(a);
+    SS_LAUNCH_CHECK();
+    SS_CUDA(cudaEventRecord(ev[1], st));
+    k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+    SS_CUDA(cudaEventRecord(ev[2], st));
+    k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+    SS_CUDA(cudaEventRecord(ev[3], st));
+    k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+    SS_CUDA(cudaEventRecord(ev[4], st));
+    k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+    SS_CUDA(cudaEventRecord(ev[5], st));
+    SS_CUDA(cudaMemcpyAsync(K->h_done, a.n_done, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaEventSynchronize(ev[5]));
+    for (int q = 0; q < 5; ++q) {
+      float ms = 0;
+      SS_CUDA(cudaEventElapsedTime(&ms, ev[q], ev[q + 1]));
+      ms_out[q] += ms;
+      launches_out[q] += 1;
+    }
+    ++tick;
+    done = K->h_done[0];
+    if (done >= a.nb) break;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return SS_OK;
+}
+
+extern "C" int ss_krylov_profile(ss_krylov* K, int nb, const double* omegas_host, double tol, int64_t maxiter,
+                                 int jacobi, void* stream_, double* ms_out, int64_t* bytes_out, int64_t* launches_out) {
+  if (!K || nb < 1 || nb > K->max_batch || !omegas_host || !ms_out || !bytes_out || !launches_out) {
+    ss_set_error("bad arguments");
+    return SS_ERR_ARG;
+  }
+  SS_CUDA(cudaSetDevice(K->device));
+  cudaStream_t st = (cudaStream_t)stream_;
+  KArgs a = K->a;
+  a.nb = nb;
+  a.jacobi = jacobi;
+  std::vector<ModeCtl> ctl(nb);
+  for (int b = 0; b < nb; ++b) {
+    ModeCtl c{};
+    c.maxiter = (int)maxiter;
+    c.restart = a.restart;
+    c.tol = tol;
+    c.omega = omegas_host[b];
+    c.set = b;
+    ctl[b] = c;
+  }
+  SS_CUDA(cudaMemcpyAsync(a.ctl, ctl.data(), sizeof(ModeCtl) * nb, cudaMemcpyHostToDevice, st));
+  SS_CUDA(cudaMemsetAsync(a.n_done, 0, sizeof(int), st));
+  SS_CUDA(cudaMemsetAsync(a.X, 0, sizeof(double2) * a.ld * nb, st));
+  SS_CUDA(cudaMemsetAsync(a.bytes, 0, sizeof(unsigned long long) * 8, st));
+  if (tick_dim(K) == 3) k_init<3><<<nb * a.nseg, PT, 0, st>>>(a);
+  else k_init<2><<<nb * a.nseg, PT, 0, st>>>(a);
+  SS_LAUNCH_CHECK();
+  for (int q = 0; q < 5; ++q) { ms_out[q] = 0; launches_out[q] = 0; }
+  const int64_t max_ticks = maxiter + 3 * (maxiter / std::max<int64_t>(1, std::min<int64_t>(a.restart, maxiter + 1)) + 2) + 16;
+  int rc = tick_dim(K) == 3 ? profile_ticks<3>(K, a, st, max_ticks, ms_out, launches_out)
+                            : profile_ticks<2>(K, a, st, max_ticks, ms_out, launches_out);
+  if (rc) return rc;
+  unsigned long long hb[8];
+  SS_CUDA(cudaMemcpyAsync(hb, a.bytes, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  for (int q = 0; q < 5; ++q) bytes_out[q] = (int64_t)hb[q];
+  return SS_OK;
+}

@@ -1,0 +1,122 @@
+// Mode-batched complex SpMV building blocks for the structured saddle operator
+//   A(w) = [[ S' (x) I + i w M' (x) I , D ], [ D^T, 0 ]]   (reference assembly.py:424-430)
+// The node-level pattern stores one (S', M') pair per free node pair and applies it to all `dim`
+// velocity components (kron structure), so the matrix stream is ~dim x smaller than the vector
+// CSR; D is stored per (node, pressure) pair as `dim` doubles, once in row order (velocity rows)
+// and once transposed (pressure rows).  w*M' is formed in registers per mode.
+#pragma once
+#include "ss_common.h"
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// Smith's complex division a / b (numpy's npy_cdiv algorithm).
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double abs_br = fabs(b.x), abs_bi = fabs(b.y);
+  if (abs_br >= abs_bi) {
+    if (abs_br == 0.0 && abs_bi == 0.0) return make_double2(a.x / abs_br, a.y / abs_bi);
+    const double rat = b.y / b.x;
+    const double scl = 1.0 / (b.x + b.y * rat);
+    return make_double2((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+  }
+  const double rat = b.x / b.y;
+  const double scl = 1.0 / (b.y + b.x * rat);
+  return make_double2((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Jacobi scale of velocity node row r at frequency w: 1/(S'_rr + i w M'_rr), 1 if that is 0
+// (krylov.py:49-60 on the reduced matrix's diagonal; the pressure diagonal is 0 -> 1).
+__device__ __forceinline__ double2 saddle_jacobi(const SsOperatorDev& op, int r, double omega) {
+  const double2 d = op.dsm[r];
+  const double2 a = make_double2(d.x, omega == 0.0 ? 0.0 : omega * d.y);
+  if (a.x == 0.0 && a.y == 0.0) return make_double2(1.0, 0.0);
+  return cdiv(make_double2(1.0, 0.0), a);
+}
+
+// One warp computes all DIM components of velocity node row r: acc[d] = (A x)_(r,d), result valid
+// in every lane after the butterfly (lane 0's value is used; the tree is fixed -> deterministic).
+template <int DIM>
+__device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, double omega,
+                                               const double2* __restrict__ x, int lane,
+                                               double2 (&acc)[DIM]) {
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
+  const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const int B = __ldg(op.ncol + e);
+    const double2 a = __ldg(op.sm + e);
+    const double am = omega * a.y;
+    const double2* xb = x + (size_t)B * DIM;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const double2 v = xb[d];
+      acc[d].x += a.x * v.x - am * v.y;
+      acc[d].y += a.x * v.y + am * v.x;
+    }
+  }
+  const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
+  for (int e = p0 + lane; e < p1; e += 32) {
+    const double2 v = x[op.nfv + __ldg(op.pcol + e)];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const double dv = __ldg(op.dp + (size_t)e * DIM + d);
+      acc[d].x += dv * v.x;
+      acc[d].y += dv * v.y;
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    acc[d].x = warp_sum(acc[d].x);
+    acc[d].y = warp_sum(acc[d].y);
+  }
+}
+
+// One warp computes pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
+template <int DIM>
+__device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int j,
+                                                   const double2* __restrict__ x, int lane) {
+  double2 acc = make_double2(0.0, 0.0);
+  const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const double2* xb = x + (size_t)__ldg(op.tcol + e) * DIM;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const double dv = __ldg(op.dt + (size_t)e * DIM + d);
+      const double2 v = xb[d];
+      acc.x += dv * v.x;
+      acc.y += dv * v.y;
+    }
+  }
+  acc.x = warp_sum(acc.x);
+  acc.y = warp_sum(acc.y);
+  return acc;
+}
+
+// Generic complex CSR row (drop-in gmres on arbitrary matrices): warp per row.
+__device__ __forceinline__ double2 csr_row(const SsCsrDev& A, int set, int row,
+                                           const double2* __restrict__ x, int lane) {
+  double2 acc = make_double2(0.0, 0.0);
+  const double2* vals = A.vals + (size_t)set * A.nnz;
+  const int e0 = __ldg(A.indptr + row), e1 = __ldg(A.indptr + row + 1);
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const double2 a = __ldg(vals + e);
+    const double2 v = x[__ldg(A.indices + e)];
+    acc.x += a.x * v.x - a.y * v.y;
+    acc.y += a.x * v.y + a.y * v.x;
+  }
+  acc.x = warp_sum(acc.x);
+  acc.y = warp_sum(acc.y);
+  return acc;
+}

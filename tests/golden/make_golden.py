@@ -1,0 +1,238 @@
+"""Generate the golden fixtures from the REFERENCE implementation itself.
+
+Run once in the build container (the only place `/root/reference` exists):
+
+    python tests/golden/make_golden.py            # all fixtures (~5 min on 8 cores)
+
+It imports the reference package read-only (`/root/reference/pkg/src/spectralstokes`), never its
+CLI/figures modules (matplotlib is absent), pins BLAS to one thread as the reference's own
+`pkg/tests/conftest.py:5-9` does, and writes compressed ``.npz`` fixtures next to this script.
+Nothing at test / bench time reads `/root/reference`; only these fixtures travel.
+
+Fixtures
+  shapes.npz      reference_shapes(2|3) tables and contracted Mref/sref/tref   (assembly.py:115-190,236)
+  meshes.npz      reference-built meshes + promoted numbering (mesh.py:241-315, structured.py)
+  c1.npz          BASELINE config 1: pattern, values, rhs, solved fields (tol 1e-10), reconstruct,
+                  fixed-budget GMRES history                                    (assembly.py:403, krylov.py:63,
+                                                                                 spectral.py:254-317)
+  pipe3d.npz      down-scaled 3D pipe (pipe_grid(3,15)), parabolic Dirichlet inlet, modes 1 and 16
+  c2_pattern.npz  BASELINE config 2 (jittered 199 800-tet pipe): pattern hash, sampled A@x and rhs
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+from multiprocessing import Pool
+from pathlib import Path
+
+os.environ["OMP_NUM_THREADS"] = "1"
+os.environ["OPENBLAS_NUM_THREADS"] = "1"
+os.environ["MKL_NUM_THREADS"] = "1"
+os.environ["PYTHONDONTWRITEBYTECODE"] = "1"
+sys.dont_write_bytecode = True
+
+import numpy as np  # noqa: E402
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(REPO))
+
+from spectralstokes import assembly as RA  # noqa: E402
+from spectralstokes import krylov as RK  # noqa: E402
+from spectralstokes import mesh as RM  # noqa: E402
+from spectralstokes import spectral as RSP  # noqa: E402
+from spectralstokes import structured as RS  # noqa: E402
+
+from paper_2009_06725_b200.workloads import (  # noqa: E402
+    C1_TOL, c1_case, c2_case, pipe3d_case,
+)
+
+
+def _sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _ref_qmesh(mesh_mine, geom_kind=None, radius=None):
+    """Rebuild a mesh with the REFERENCE classes and promote it with the reference."""
+    patches = {n: RM.BoundaryPatch(kind=p.kind, faces=np.asarray(p.faces)) for n, p in mesh_mine.boundary_patches.items()}
+    rmesh = RM.Mesh(np.asarray(mesh_mine.nodes), np.asarray(mesh_mine.elements), patches)
+    geom = None
+    if geom_kind == "cylinder":
+        geom = RM.BoundaryGeometry(surfaces={"wall": RM.CylinderBoundary(point=(0.0, 0.0, 0.0), axis=(0.0, 0.0, 1.0), radius=radius)})
+    return RM.promote_to_quadratic(rmesh, geom)
+
+
+def _mesh_arrays(prefix, q):
+    out = {f"{prefix}_nodes": q.nodes, f"{prefix}_elements": q.elements, f"{prefix}_vel_conn": q.vel_conn,
+           f"{prefix}_edges": q.edges, f"{prefix}_nvert": np.int64(q.n_vertices)}
+    names = sorted(q.boundary_patches)
+    out[f"{prefix}_patch_names"] = np.array(names)
+    for n in names:
+        p = q.boundary_patches[n]
+        out[f"{prefix}_patch_{n}_kind"] = np.array(p.kind)
+        out[f"{prefix}_patch_{n}_faces"] = p.faces
+        out[f"{prefix}_patch_{n}_face_conn"] = p.face_conn
+    return out
+
+
+def make_shapes():
+    out = {}
+    for dim in (2, 3):
+        s = RA.reference_shapes(dim)
+        out[f"d{dim}_points"] = s.points
+        out[f"d{dim}_weights"] = s.weights
+        out[f"d{dim}_vel_values"] = s.vel_values
+        out[f"d{dim}_vel_grads"] = s.vel_grads
+        out[f"d{dim}_pres_values"] = s.pres_values
+        out[f"d{dim}_mref"] = np.einsum("q,qa,qb->ab", s.weights, s.vel_values, s.vel_values)
+        out[f"d{dim}_sref"] = np.einsum("q,qam,qbn->abmn", s.weights, s.vel_grads, s.vel_grads)
+        out[f"d{dim}_tref"] = np.einsum("q,qam,qb->amb", s.weights, s.vel_grads, s.pres_values)
+    np.savez_compressed(HERE / "shapes.npz", **out)
+
+
+def make_meshes():
+    out = {}
+    for name, (nx, ny, L, H) in {"chan10x4": (10, 4, 4.0, 1.0), "chan3x2": (3, 2, 2.0, 1.0)}.items():
+        q = RM.promote_to_quadratic(RS.channel_grid(nx, ny, L, H))
+        out.update(_mesh_arrays(name, q))
+    for name, (nr, nl) in {"pipe2x3": (2, 3), "pipe3x4": (3, 4)}.items():
+        m, g = RS.pipe_grid(nr, nl, 0.5, 5.0)
+        out.update(_mesh_arrays(name, RM.promote_to_quadratic(m, g)))
+    np.savez_compressed(HERE / "meshes.npz", **out)
+
+
+# -- config 1 ------------------------------------------------------------------------------------
+
+def _c1_setup():
+    case = c1_case()
+    q = _ref_qmesh(case.mesh)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    wf = RSP.BoundaryWaveform(patch="inlet", kind="neumann", direction=np.array([1.0, 0.0]),
+                              period=case.period, coefficients=case.coefficients)
+    ms = RSP.fourier_transform_bcs([wf], case.n_modes)
+    return case, q, props, ms
+
+
+def _c1_solve(idx):
+    case, q, props, ms = _c1_setup()
+    t0 = time.perf_counter()
+    sol = RSP._solve_one_mode(q, props, ms, RK.SolverSettings(tolerance=C1_TOL, restart=200), idx, "full")
+    return idx, sol.velocity, sol.pressure, sol.report.iterations, sol.report.residual, sol.report.converged, time.perf_counter() - t0
+
+
+def make_c1(pool):
+    case, q, props, ms = _c1_setup()
+    out = _mesh_arrays("mesh", q)
+    out["coefficients"] = case.coefficients
+    out["omegas"] = ms.frequencies
+    patterns = []
+    for i, om in enumerate(ms.frequencies):
+        s = RA.assemble_mode_system(q, props, float(om), h_mode={"inlet": ms.coefficients["inlet"][i] * np.array([1.0, 0.0])})
+        patterns.append((s.matrix.indptr.copy(), s.matrix.indices.copy()))
+        out[f"rhs_{i}"] = s.rhs
+        if i == 1:
+            out["indptr"], out["indices"] = s.matrix.indptr, s.matrix.indices
+            out["data_1"] = s.matrix.data
+            out["vel_dof"], out["pres_dof"] = s.vel_dof, s.pres_dof
+            out["jacobi_1"] = RK.jacobi_precondition(s)
+            rng = np.random.default_rng(1234)
+            x = rng.normal(size=s.n_dofs) + 1j * rng.normal(size=s.n_dofs)
+            out["spmv_x"], out["spmv_y"] = x, s.matrix @ x
+            xb, it, hist, conv = RK.gmres(s.matrix, s.rhs, tol=C1_TOL, restart=200, maxiter=200, scale=RK.jacobi_precondition(s))
+            out["budget_x"], out["budget_hist"] = xb, np.array(hist)
+            xb, it, hist, conv = RK.gmres(s.matrix, s.rhs, tol=C1_TOL, restart=40, maxiter=100, scale=RK.jacobi_precondition(s))
+            out["budget40_x"], out["budget40_hist"] = xb, np.array(hist)
+    out["pattern_same_all_omega"] = np.bool_(all(np.array_equal(a[0], patterns[0][0]) and np.array_equal(a[1], patterns[0][1]) for a in patterns))
+    res = sorted(pool.map(_c1_solve, range(case.n_modes + 1)))
+    sols = []
+    for idx, u, p, it, r, conv, wall in res:
+        out[f"u_{idx}"], out[f"p_{idx}"] = u, p
+        out[f"iters_{idx}"], out[f"res_{idx}"], out[f"conv_{idx}"], out[f"wall_{idx}"] = it, r, conv, wall
+        sols.append(RSP.ModeSolution(index=idx, omega=float(ms.frequencies[idx]), velocity=u, pressure=p,
+                                     report=RK.SolveReport(iterations=it, residual=r, converged=conv, wall_time=wall)))
+    ts = np.array([0, 5, 13, 27]) / 32.0
+    out["recon_t"] = ts
+    for j, t in enumerate(ts):
+        out[f"recon_u_{j}"], out[f"recon_p_{j}"] = RSP.reconstruct(sols, float(t))
+    np.savez_compressed(HERE / "c1.npz", **out)
+    print("c1 iterations", [r[3] for r in res], "wall", sum(r[6] for r in res))
+
+
+# -- down-scaled 3D pipe ---------------------------------------------------------------------------
+
+def _pipe_solve(idx):
+    case = pipe3d_case()
+    q = _ref_qmesh(case.mesh, "cylinder", case.radius)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    g = case.coefficients[idx] * case.profile
+    s = RA.assemble_mode_system(q, props, float(case.omegas[idx]), g_mode=g)
+    t0 = time.perf_counter()
+    x, rep = RK.gmres_solve(s, RK.SolverSettings(tolerance=C1_TOL, restart=200))
+    u, p = s.expand(x)
+    return idx, u, p, rep.iterations, rep.residual, rep.converged, time.perf_counter() - t0, s
+
+
+def make_pipe3d(pool):
+    case = pipe3d_case()
+    q = _ref_qmesh(case.mesh, "cylinder", case.radius)
+    out = _mesh_arrays("mesh", q)
+    out["profile"], out["coefficients"], out["omegas"] = case.profile, case.coefficients, case.omegas
+    picks = [1, 16]
+    res = pool.map(_pipe_solve, picks)
+    for idx, u, p, it, r, conv, wall, s in res:
+        out[f"u_{idx}"], out[f"p_{idx}"] = u, p
+        out[f"iters_{idx}"], out[f"res_{idx}"], out[f"conv_{idx}"], out[f"wall_{idx}"] = it, r, conv, wall
+        out[f"rhs_{idx}"] = s.rhs
+        out[f"pattern_sha_{idx}"] = np.array(_sha(s.matrix.indptr, s.matrix.indices))
+        out[f"nnz_{idx}"] = np.int64(s.matrix.nnz)
+    np.savez_compressed(HERE / "pipe3d.npz", **out)
+    print("pipe3d iterations", [(r[0], r[3]) for r in res])
+
+
+# -- config 2 pattern --------------------------------------------------------------------------------
+
+def make_c2_pattern():
+    case = c2_case()
+    t0 = time.perf_counter()
+    q = _ref_qmesh(case.mesh, "cylinder", case.radius)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    out = {"mesh_nodes_sha": np.array(_sha(q.nodes)), "mesh_conn_sha": np.array(_sha(q.vel_conn))}
+    rng = np.random.default_rng(99)
+    for idx in (0, 1):
+        g = case.coefficients[idx] * case.profile
+        s = RA.assemble_mode_system(q, props, float(case.omegas[idx]), g_mode=g)
+        out[f"pattern_sha_{idx}"] = np.array(_sha(s.matrix.indptr, s.matrix.indices))
+        out[f"nnz_{idx}"] = np.int64(s.matrix.nnz)
+        out["n"] = np.int64(s.n_dofs)
+        x = rng.normal(size=s.n_dofs) + 1j * rng.normal(size=s.n_dofs)
+        y = s.matrix @ x
+        rows = np.sort(np.random.default_rng(7).choice(s.n_dofs, 2000, replace=False))
+        out[f"spmv_seed_{idx}"] = np.int64(99)
+        out[f"spmv_rows_{idx}"], out[f"spmv_y_{idx}"], out[f"spmv_norm_{idx}"] = rows, y[rows], np.linalg.norm(y)
+        out[f"rhs_rows_{idx}"], out[f"rhs_norm_{idx}"] = s.rhs[rows], np.linalg.norm(s.rhs)
+        out[f"diag_rows_{idx}"] = s.matrix.diagonal()[rows]
+        rng = np.random.default_rng(99)
+    np.savez_compressed(HERE / "c2_pattern.npz", **out)
+    print("c2 pattern", time.perf_counter() - t0, "s")
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d"]
+    with Pool(min(9, os.cpu_count() or 1)) as pool:
+        if "shapes" in what:
+            make_shapes()
+        if "meshes" in what:
+            make_meshes()
+        if "c2" in what:
+            make_c2_pattern()
+        if "c1" in what:
+            make_c1(pool)
+        if "pipe3d" in what:
+            make_pipe3d(pool)
