@@ -385,14 +385,28 @@ class ModeSystemBatch:
         return len(self.omegas)
 
 
-def assemble_mode_systems(qmesh, props: FluidProps, omegas, g_modes=None, h_modes=None, operator=None):
-    """Batched ``assemble_mode_system`` for many modes at once (one device RHS launch)."""
+def assemble_mode_systems(qmesh, props: FluidProps, omegas, g_modes=None, h_modes=None, operator=None,
+                          g_device=None):
+    """Batched ``assemble_mode_system`` for many modes at once (one device RHS launch).
+
+    ``g_device`` optionally supplies the nodal Dirichlet data of all modes as a device tensor
+    (nb, n_vel_nodes, dim) complex128 that the caller guarantees is zero off constrained nodes
+    (the zero-copy path used by the end-to-end benchmark); it replaces ``g_modes``.
+    """
     torch = _lib.torch_mod()
     omegas = np.asarray(omegas, dtype=float).reshape(-1)
     if np.any(omegas < 0):
         raise ValueError("omega must be non-negative")
     nb = omegas.size
     op = operator or get_operator(qmesh, props)
+    if g_device is not None:
+        if tuple(g_device.shape) != (nb, qmesh.n_velocity_nodes, qmesh.dim) or g_device.dtype != torch.complex128:
+            raise ValueError("g_device must be (nb, n_velocity_nodes, dim) complex128")
+        loads = None
+        if h_modes is not None and any(h for h in h_modes):
+            host = np.stack([_traction_loads(qmesh, h) for h in h_modes])
+            loads = torch.from_numpy(host).to(op.device)
+        return ModeSystemBatch(op, omegas, op.rhs(omegas, loads, g_device), g_device, [None] * nb)
     gl = [None] * nb if g_modes is None else [_nodal_dirichlet(qmesh, g) for g in g_modes]
     hl = [None] * nb if h_modes is None else list(h_modes)
     for g in gl:

@@ -411,30 +411,17 @@ extern "C" int ss_jacobi(const ss_pattern* P, int nb, const double* omegas_dev, 
 // One warp per node row (all dim components) or pressure row; blockIdx.y = mode.
 // ------------------------------------------------------------------------------------------------
 template <int DIM>
-__global__ void __launch_bounds__(256) k_spmv_saddle(SsOperatorDev op, const double* __restrict__ omegas,
+__global__ void __launch_bounds__(256) k_spmv_saddle(SsOperatorDev op, int nb, const double* __restrict__ omegas,
                                                      const double2* __restrict__ X, double2* __restrict__ Y,
                                                      int64_t ld, int jacobi) {
-  const int lane = threadIdx.x & 31;
-  const int task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int b = blockIdx.y;
+  const int b = blockIdx.x % nb, blk = blockIdx.x / nb;   // mode fastest: the matrix block is shared in L2
   const double om = omegas[b];
   const double2* x = X + (size_t)b * ld;
   double2* y = Y + (size_t)b * ld;
-  if (task < op.nfree) {
-    double2 acc[DIM];
-    saddle_vel_row<DIM>(op, task, om, x, lane, acc);
-    if (lane < DIM) {
-      double2 v = acc[0];
-#pragma unroll
-      for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
-      if (jacobi) v = cmul(saddle_jacobi(op, task, om), v);
-      y[(size_t)task * DIM + lane] = v;
-    }
-  } else if (task < op.nfree + op.npf) {
-    const int j = task - op.nfree;
-    const double2 v = saddle_pres_row<DIM>(op, j, x, lane);
-    if (lane == 0) y[op.nfv + j] = v;
-  }
+  saddle_block<DIM>(op, blk, om, x, [&](int row, double2 v) {
+    if (jacobi && row < op.nfv) v = cmul(saddle_jacobi(op, row / DIM, om), v);
+    y[row] = v;
+  });
 }
 
 extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas_dev, const double* x_dev,
@@ -442,12 +429,11 @@ extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas
   if (!P || !x_dev || !y_dev || !omegas_dev || nb <= 0 || ld < P->op.n) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
   if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
   cudaStream_t st = (cudaStream_t)stream_;
-  const int tasks = P->nfree + P->npf;
-  dim3 grid((tasks + 7) / 8, nb);
+  const unsigned grid = (unsigned)(saddle_nsb_host(P->nfree, P->npf) * nb);
   if (P->dim == 2)
-    k_spmv_saddle<2><<<grid, 256, 0, st>>>(P->op, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
+    k_spmv_saddle<2><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
   else
-    k_spmv_saddle<3><<<grid, 256, 0, st>>>(P->op, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
+    k_spmv_saddle<3><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
@@ -468,40 +454,21 @@ extern "C" int64_t ss_spmv_bytes(const ss_pattern* P, int nb) {
 // fixed order -> deterministic.
 // ------------------------------------------------------------------------------------------------
 template <int DIM>
-__global__ void __launch_bounds__(256) k_resid_partials(SsOperatorDev op, const double* __restrict__ omegas,
+__global__ void __launch_bounds__(256) k_resid_partials(SsOperatorDev op, int nb, const double* __restrict__ omegas,
                                                         const double2* __restrict__ B, const double2* __restrict__ X,
                                                         int64_t ld, double2* __restrict__ part) {
   __shared__ double red[2][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.y;
+  const int b = blockIdx.x % nb, blk = blockIdx.x / nb;
   const double om = omegas[b];
   const double2* x = X + (size_t)b * ld;
   const double2* rb = B + (size_t)b * ld;
   double tt = 0, bb = 0;
-  const int tasks = op.nfree + op.npf;
-  for (int ti = 0; ti < 8; ++ti) {
-    const int task = (blockIdx.x * 8 + warp) * 8 + ti;
-    if (task >= tasks) break;
-    if (task < op.nfree) {
-      double2 acc[DIM];
-      saddle_vel_row<DIM>(op, task, om, x, lane, acc);
-      if (lane < DIM) {
-        double2 v = acc[0];
-#pragma unroll
-        for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
-        const double2 r = rb[task * DIM + lane];
-        tt += cabs2(csub(r, v));
-        bb += cabs2(r);
-      }
-    } else {
-      const double2 v = saddle_pres_row<DIM>(op, task - op.nfree, x, lane);
-      if (lane == 0) {
-        const double2 r = rb[op.nfv + task - op.nfree];
-        tt += cabs2(csub(r, v));
-        bb += cabs2(r);
-      }
-    }
-  }
+  saddle_block<DIM>(op, blk, om, x, [&](int row, double2 v) {
+    const double2 r = rb[row];
+    tt += cabs2(csub(r, v));
+    bb += cabs2(r);
+  });
   tt = warp_sum(tt);
   bb = warp_sum(bb);
   if (lane == 0) { red[0][warp] = tt; red[1][warp] = bb; }
@@ -509,7 +476,7 @@ __global__ void __launch_bounds__(256) k_resid_partials(SsOperatorDev op, const 
   if (threadIdx.x == 0) {
     double s0 = 0, s1 = 0;
     for (int w = 0; w < 8; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
-    part[(size_t)b * gridDim.x + blockIdx.x] = make_double2(s0, s1);
+    part[(size_t)b * (gridDim.x / nb) + blk] = make_double2(s0, s1);
   }
 }
 
@@ -517,15 +484,14 @@ extern "C" int ss_residual_norms(const ss_pattern* P, int nb, const double* omeg
                                  const double* x_dev, int64_t ld, double* out_host, void* stream_) {
   if (!P || nb < 1 || !omegas_dev || !rhs_dev || !x_dev || !out_host || ld < P->op.n) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)stream_;
-  const int tasks = P->nfree + P->npf;
-  const int nblk = (tasks + 63) / 64;
+  const int nblk = saddle_nsb_host(P->nfree, P->npf);
   double2* part = nullptr;
   SS_CUDA(cudaMallocAsync((void**)&part, sizeof(double2) * nblk * nb, st));
-  dim3 grid(nblk, nb);
+  const unsigned grid = (unsigned)(nblk * nb);
   if (P->dim == 2)
-    k_resid_partials<2><<<grid, 256, 0, st>>>(P->op, omegas_dev, (const double2*)rhs_dev, (const double2*)x_dev, ld, part);
+    k_resid_partials<2><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)rhs_dev, (const double2*)x_dev, ld, part);
   else
-    k_resid_partials<3><<<grid, 256, 0, st>>>(P->op, omegas_dev, (const double2*)rhs_dev, (const double2*)x_dev, ld, part);
+    k_resid_partials<3><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)rhs_dev, (const double2*)x_dev, ld, part);
   SS_LAUNCH_CHECK();
   std::vector<double2> h((size_t)nblk * nb);
   SS_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double2) * h.size(), cudaMemcpyDeviceToHost, st));

@@ -40,7 +40,11 @@ struct ModeCtl {
 };
 
 constexpr int PT = 256;        // threads per CTA for every Krylov kernel
-constexpr int SPMV_TPW = 8;    // warp tasks (rows) per warp in the tick SpMV
+constexpr int PASS_STAGE_TARGET = 3456;   // double2 per pipeline stage (~54 KB) for small J
+constexpr int PASS_MAX_STAGES = 8;
+constexpr int PASS_STAGE_DIV = 4;         // aim for >= 4 stages in the ring
+constexpr int PASS_L2_AHEAD = 4;          // chunks prefetched into L2 beyond the smem ring
+constexpr int PASS_SMEM_ELEMS = 13440;    // dynamic shared memory of a basis pass (210 KB)
 
 struct KArgs {
   int kind;                    // 0 saddle, 1 csr
@@ -48,13 +52,15 @@ struct KArgs {
   int64_t ld;
   int nseg, seg_rows;          // pass segmentation (depends on n only)
   int nsb;                     // spmv blocks per mode
-  int cap;                     // double2 capacity of one smem stage
+  int smem_elems;              // double2 capacity of the basis-pass pipeline ring
   int jacobi;
   int64_t hist_cap;
   SsOperatorDev op;
   SsCsrDev csr;
   ModeCtl* ctl;
   double2 *Q, *W, *X, *RHS;
+  double2* P;                  // current raw basis vector q_k in row layout (SpMV input)
+  int nblk;                    // ld / RB row blocks; Q is row-block-major: [b][blk][jcap][RB]
   double* qs;                  // [b][jcap] scale of raw basis vectors
   double2 *H, *G, *CS, *SN, *C1, *C2, *Y;
   double2* part;               // [b][nseg][jcap] pass partials
@@ -65,8 +71,16 @@ struct KArgs {
   unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
 };
 
-__device__ __forceinline__ double2* qvec(const KArgs& a, int b, int j) {
-  return a.Q + ((size_t)b * a.jcap + j) * a.ld;
+constexpr int RB = 32;         // rows per block of the row-block-major basis layout
+
+// Basis storage is row-block-major: for every block of RB rows the J basis vectors are
+// contiguous (J x 512 B), so a basis pass streams long contiguous runs from HBM and moves a
+// whole block with ONE bulk-TMA copy.
+__device__ __forceinline__ double2* qblock(const KArgs& a, int b, int blk) {
+  return a.Q + ((size_t)b * a.nblk + blk) * a.jcap * RB;
+}
+__device__ __forceinline__ double2& qat(const KArgs& a, int b, int j, int64_t row) {
+  return qblock(a, b, (int)(row / RB))[(size_t)j * RB + (row % RB)];
 }
 
 // Last-CTA election: returns true in every thread of the CTA that finished last for this mode.
@@ -166,8 +180,7 @@ template <int DIM>
 __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   __shared__ double red[2][PT / 32];
   __shared__ int sflag;
-  const int b = blockIdx.x / a.nsb, sb = blockIdx.x % a.nsb;
-  if (b >= a.nb) return;
+  const int b = blockIdx.x % a.nb, sb = blockIdx.x / a.nb;   // mode fastest: one row block's CTAs co-run
   ModeCtl* c = a.ctl + b;
   const int phase = c->phase;
   if (phase != PH_INNER && phase != PH_START && phase != PH_RESID) return;
@@ -175,53 +188,26 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double om = c->omega;
   const int k = c->k;
-  const double2* x = resid ? a.X + (size_t)b * a.ld : qvec(a, b, k);
+  const double2* x = (resid ? a.X : a.P) + (size_t)b * a.ld;
   const double xs = resid ? 1.0 : a.qs[b * a.jcap + k];
-  double2* out = resid ? qvec(a, b, 0) : a.W + (size_t)b * a.ld;
+  double2* out = resid ? a.P + (size_t)b * a.ld : a.W + (size_t)b * a.ld;
   const double2* rhs = a.RHS + (size_t)b * a.ld;
   double tt = 0, rr = 0;
-  const int tasks = a.kind == 0 ? a.op.nfree + a.op.npf : a.n;
-  const int t0 = (sb * (PT / 32) + warp) * SPMV_TPW;
-  for (int ti = 0; ti < SPMV_TPW; ++ti) {
-    const int task = t0 + ti;
-    if (task >= tasks) break;
-    if (a.kind == 0 && task < a.op.nfree) {
-      double2 acc[DIM];
-      saddle_vel_row<DIM>(a.op, task, om, x, lane, acc);
-      const double2 s = a.jacobi ? saddle_jacobi(a.op, task, om) : make_double2(1.0, 0.0);
-      if (lane < DIM) {
-        double2 v = acc[0];
-#pragma unroll
-        for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
-        const int row = task * DIM + lane;
-        if (resid) {
-          const double2 t = csub(rhs[row], v);
-          const double2 r = cmul(s, t);
-          out[row] = r;
-          tt += cabs2(t);
-          rr += cabs2(r);
-        } else {
-          out[row] = cmul(s, cscale(v, xs));
-        }
-      }
+  auto emit = [&](int row, double2 v) {
+    const double2 s = row_scale<DIM>(a, b, row, om);
+    if (resid) {
+      const double2 t = csub(rhs[row], v);
+      const double2 r = cmul(s, t);
+      out[row] = r;
+      qat(a, b, 0, row) = r;
+      tt += cabs2(t);
+      rr += cabs2(r);
     } else {
-      const int row = a.kind == 0 ? a.op.nfv + (task - a.op.nfree) : task;
-      const double2 v = a.kind == 0 ? saddle_pres_row<DIM>(a.op, task - a.op.nfree, x, lane)
-                                    : csr_row(a.csr, a.csr.nvals > 1 ? b : 0, task, x, lane);
-      if (lane == 0) {
-        const double2 s = a.kind == 0 ? make_double2(1.0, 0.0) : row_scale<DIM>(a, b, row, om);
-        if (resid) {
-          const double2 t = csub(rhs[row], v);
-          const double2 r = cmul(s, t);
-          out[row] = r;
-          tt += cabs2(t);
-          rr += cabs2(r);
-        } else {
-          out[row] = cmul(s, cscale(v, xs));
-        }
-      }
+      out[row] = cmul(s, cscale(v, xs));
     }
-  }
+  };
+  if (a.kind == 0) saddle_block<DIM>(a.op, sb, om, x, emit);
+  else csr_block(a.csr, a.csr.nvals > 1 ? b : 0, sb, x, emit);
   if (resid) {
     tt = warp_sum(tt);
     rr = warp_sum(rr);
@@ -303,14 +289,176 @@ __device__ __forceinline__ int pow2floor(int v) {
   return p;
 }
 
+__device__ __forceinline__ void cp_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_wait<0>(); break;
+    case 1: cp_wait<1>(); break;
+    case 2: cp_wait<2>(); break;
+    case 3: cp_wait<3>(); break;
+    case 4: cp_wait<4>(); break;
+    case 5: cp_wait<5>(); break;
+    case 6: cp_wait<6>(); break;
+    default: cp_wait<7>(); break;
+  }
+}
+
+// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
+__device__ __forceinline__ int pass_slices(int nr) { return nr > 4 ? 1 : nr > 2 ? 2 : nr > 1 ? 4 : 8; }
+
+// Streams one segment (SEGB row blocks) of one mode's basis through a ring of shared-memory
+// stages filled by bulk TMA (one copy per row block: J x 512 B contiguous, one for the vector).
+//   phase 1 (B, C, X): V <- V -/+ sum_j S_j c_j   warps = (block, j-slice), lanes = rows
+//   phase 2 (A, B):    acc_t += conj(S_{warp+8t}) V   per-lane register accumulators
+// Writes this CTA's partials: part[j] (A, B) or part[0].x = ||w||^2 (C).
+template <int PASS, int T>
+__device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int J, int k, const double2* coef,
+                                               double2* smem, uint64_t* mbar, double2* red, double2* part) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int segb = a.seg_rows / RB;
+  const int blk_begin = s * segb;
+  const int blk_end = min(blk_begin + segb, a.nblk);
+  const int nblocks = blk_end - blk_begin;
+  const int belem = J * RB;
+  const int CB = max(1, min(min(nblocks, 8), (a.smem_elems / 3) / (belem + RB)));
+  const int stage_elems = CB * (belem + RB);
+  const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
+  const int nchunks = (nblocks + CB - 1) / CB;
+  double2* vec = (PASS == PASS_X ? a.X : a.W) + (size_t)b * a.ld;
+  auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
+  auto load_chunk = [&](int ci) {   // single producer thread
+    double2* st = stage(ci);
+    const int c0 = blk_begin + ci * CB;
+    const int nc = min(CB, blk_end - c0);
+    uint64_t* bar = &mbar[ci % NS];
+    mbar_expect_tx(bar, (unsigned)(nc * (belem + RB) * 16));
+    for (int c = 0; c < nc; ++c) bulk_g2s(st + c * belem, qblock(a, b, c0 + c), (unsigned)belem * 16u, bar);
+    bulk_g2s(st + CB * belem, vec + (size_t)c0 * RB, (unsigned)(nc * RB * 16), bar);
+  };
+  if (tid < PASS_MAX_STAGES) mbar_init(&mbar[tid], 1);
+  fence_mbar_init();
+  __syncthreads();
+  if (tid == 0)
+    for (int ci = 0; ci < NS - 1 && ci < nchunks; ++ci) load_chunk(ci);
+  double2 acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
+  double nrm = 0.0;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    if (tid == 0 && ci + NS - 1 < nchunks) load_chunk(ci + NS - 1);   // stage of chunk ci-1 (released)
+    mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
+    double2* st = stage(ci);
+    const int c0 = blk_begin + ci * CB;
+    const int nc = min(CB, blk_end - c0);
+    double2* Vb = st + CB * belem;
+    if (PASS != PASS_A) {
+      for (int cr = 0; cr < nc; cr += 8) {
+        const int nr = min(8, nc - cr);
+        const int SL = pass_slices(nr);
+        const int cl = warp / SL, sl = warp % SL;
+        double2 p = make_double2(0.0, 0.0);
+        if (cl < nr) {
+          const double2* S = st + (cr + cl) * belem + lane;
+          for (int j = sl; j < J; j += SL) {
+            const double2 q = S[j * RB], cf = coef[j];
+            p.x += q.x * cf.x - q.y * cf.y;
+            p.y += q.x * cf.y + q.y * cf.x;
+          }
+        }
+        red[tid] = p;
+        __syncthreads();
+        if (sl == 0 && cl < nr) {
+          double2 tot = p;
+          for (int q = 1; q < SL; ++q) tot = cadd(tot, red[tid + 32 * q]);
+          const int c = cr + cl;
+          const double2 v = PASS == PASS_X ? cadd(Vb[c * RB + lane], tot) : csub(Vb[c * RB + lane], tot);
+          Vb[c * RB + lane] = v;
+          const int64_t row = (int64_t)(c0 + c) * RB + lane;
+          if (PASS == PASS_C) {
+            qblock(a, b, c0 + c)[(size_t)(k + 1) * RB + lane] = v;   // raw q_{k+1}
+            a.P[(size_t)b * a.ld + row] = v;
+            nrm += cabs2(v);
+          } else {
+            vec[row] = v;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (PASS == PASS_A || PASS == PASS_B) {
+      for (int c = 0; c < nc; ++c) {
+        const double2* S = st + c * belem + lane;
+        const double2 v = Vb[c * RB + lane];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int j = warp + 8 * t;
+          if (j < J) {
+            const double2 q = S[j * RB];
+            acc[t].x += q.x * v.x + q.y * v.y;
+            acc[t].y += q.x * v.y - q.y * v.x;
+          }
+        }
+      }
+    }
+    fence_proxy_async();   // generic-proxy smem writes before the async proxy refills this stage
+    __syncthreads();
+  }
+  if (tid == 0 && blk_begin * RB < a.n) {
+    // algorithmic bytes of this CTA: J basis rows read + vector read (+ vector/basis row written)
+    const int64_t real_rows = min((int64_t)blk_end * RB, (int64_t)a.n) - (int64_t)blk_begin * RB;
+    atomicAdd(a.bytes + PASS, (unsigned long long)((J + (PASS == PASS_A ? 1 : 2)) * real_rows * 16));
+  }
+  if (PASS == PASS_A || PASS == PASS_B) {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int j = warp + 8 * t;
+      const double x = warp_sum(acc[t].x), y = warp_sum(acc[t].y);
+      if (lane == 0 && j < J) part[j] = make_double2(x, y);
+    }
+  } else if (PASS == PASS_C) {
+    red[tid] = make_double2(nrm, 0.0);
+    __syncthreads();
+    for (int o = PT / 2; o > 0; o >>= 1) {
+      if (tid < o) red[tid].x += red[tid + o].x;
+      __syncthreads();
+    }
+    if (tid == 0) part[0] = red[0];
+  }
+}
+
 template <int PASS>
 __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
-  extern __shared__ __align__(16) double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
   __shared__ double2 coef[256];
   __shared__ double2 red[PT];
+  __shared__ __align__(8) uint64_t mbar[PASS_MAX_STAGES];
   __shared__ int sflag;
-  const int b = blockIdx.x / a.nseg, s = blockIdx.x % a.nseg;
-  if (b >= a.nb) return;
+  const int b = blockIdx.x % a.nb, s = blockIdx.x / a.nb;
   ModeCtl* c = a.ctl + b;
   const int phase = c->phase;
   if (PASS == PASS_X ? phase != PH_XUPDATE : phase != PH_INNER) return;
@@ -325,128 +473,22 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   } else if (PASS == PASS_X) {
     for (int j = tid; j < J; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
   }
-  const int Tj = J > 0 ? max(1, pow2floor(PT / J)) : 1;
-  int m = (a.cap - J * Tj) / (32 * (J + 1));
-  m = max(1, min(m, a.seg_rows / 32));
-  const int R = 32 * m;
-  const int stride = R + Tj;
-  const int stage_elems = J * stride + R;
-  double2* stage[2] = {smem, smem + a.cap};
-  const int64_t row_begin = (int64_t)s * a.seg_rows;
-  const int64_t row_end = min(row_begin + a.seg_rows, a.ld);
-  const int nchunks = (int)((row_end - row_begin + R - 1) / R);
-  double2* vec = (PASS == PASS_X ? a.X : a.W) + (size_t)b * a.ld;
-  const double2* Qb = a.Q + (size_t)b * a.jcap * a.ld;
-
-  auto load_chunk = [&](int ci, double2* st) {
-    const int64_t r0 = row_begin + (int64_t)ci * R;
-    const int rows = (int)min((int64_t)R, row_end - r0);
-    const int total = J * rows;
-    for (int idx = tid; idx < total; idx += PT) {
-      const int j = idx / rows, r = idx - j * rows;
-      cp16(st + j * stride + r, Qb + (size_t)j * a.ld + r0 + r);
-    }
-    for (int r = tid; r < rows; r += PT) cp16(st + J * stride + r, vec + r0 + r);
-    cp_commit();
-  };
-
-  double2 dot = make_double2(0.0, 0.0);   // phase-2 accumulator of thread (j = tid/Tj, sub = tid%Tj)
-  double nrm = 0.0;                        // pass C: ||w||^2 of rows this thread finalises
-  const int my_j = tid / Tj, my_sub = tid % Tj;
-  if (J > 0) load_chunk(0, stage[0]);
   __syncthreads();
-  for (int ci = 0; ci < nchunks; ++ci) {
-    double2* st = stage[ci & 1];
-    if (ci + 1 < nchunks) {
-      load_chunk(ci + 1, stage[(ci + 1) & 1]);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const int64_t r0 = row_begin + (int64_t)ci * R;
-    const int rows = (int)min((int64_t)R, row_end - r0);
-    double2* V = st + J * stride;
-    if (PASS != PASS_A) {
-      // phase 1: V[r] (+/-)= sum_j S[j][r] coef[j]
-      if (rows >= PT) {
-        for (int r = tid; r < rows; r += PT) {
-          double2 acc = make_double2(0.0, 0.0);
-          for (int j = 0; j < J; ++j) {
-            const double2 q = st[j * stride + r], cf = coef[j];
-            acc.x += q.x * cf.x - q.y * cf.y;
-            acc.y += q.x * cf.y + q.y * cf.x;
-          }
-          const double2 v = PASS == PASS_X ? cadd(V[r], acc) : csub(V[r], acc);
-          V[r] = v;
-          if (PASS == PASS_C) nrm += cabs2(v);
-        }
-      } else {
-        const int JS = PT / rows;
-        const int r = tid % rows, js = tid / rows;
-        if (js < JS) {
-          double2 acc = make_double2(0.0, 0.0);
-          for (int j = js; j < J; j += JS) {
-            const double2 q = st[j * stride + r], cf = coef[j];
-            acc.x += q.x * cf.x - q.y * cf.y;
-            acc.y += q.x * cf.y + q.y * cf.x;
-          }
-          red[js * rows + r] = acc;
-        }
-        __syncthreads();
-        if (tid < rows) {
-          double2 acc = red[tid];
-          for (int q = 1; q < JS; ++q) acc = cadd(acc, red[q * rows + tid]);
-          const double2 v = PASS == PASS_X ? cadd(V[tid], acc) : csub(V[tid], acc);
-          V[tid] = v;
-          if (PASS == PASS_C) nrm += cabs2(v);
-        }
-      }
-      __syncthreads();
-      // write back the updated vector (w for B, Q[k+1] raw for C, x for X)
-      double2* dst = PASS == PASS_C ? qvec(a, b, k + 1) : vec;
-      for (int r = tid; r < rows; r += PT) dst[r0 + r] = V[r];
-    }
-    if (PASS == PASS_A || PASS == PASS_B) {
-      // phase 2: dot[j] += sum_r conj(S[j][r]) V[r]
-      if (my_j < J) {
-        for (int r = my_sub; r < rows; r += Tj) {
-          const double2 q = st[my_j * stride + r], v = V[r];
-          dot.x += q.x * v.x + q.y * v.y;
-          dot.y += q.x * v.y - q.y * v.x;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0 && row_begin < a.n) {
-    // algorithmic bytes of this CTA: J basis rows read + vector read (+ vector/basis row written)
-    const int64_t real_rows = min(row_end, (int64_t)a.n) - row_begin;
-    atomicAdd(a.bytes + PASS, (unsigned long long)((J + (PASS == PASS_A ? 1 : 2)) * real_rows * 16));
+  double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
+  const int T = (J + 7) / 8;
+  if (PASS == PASS_A || PASS == PASS_B) {
+    if (T <= 2) stream_segment<PASS, 2>(a, b, s, J, k, coef, smem, mbar, red, part);
+    else if (T <= 4) stream_segment<PASS, 4>(a, b, s, J, k, coef, smem, mbar, red, part);
+    else if (T <= 8) stream_segment<PASS, 8>(a, b, s, J, k, coef, smem, mbar, red, part);
+    else if (T <= 16) stream_segment<PASS, 16>(a, b, s, J, k, coef, smem, mbar, red, part);
+    else stream_segment<PASS, 32>(a, b, s, J, k, coef, smem, mbar, red, part);
+  } else {
+    stream_segment<PASS, 1>(a, b, s, J, k, coef, smem, mbar, red, part);
   }
   if (PASS == PASS_X) {
     if (!last_cta(a, b, PASS, a.nseg, &sflag)) return;
     if (tid == 0) c->phase = PH_RESID;
     return;
-  }
-  // per-CTA partials
-  double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
-  if (PASS == PASS_C) {
-    red[tid] = make_double2(nrm, 0.0);
-    __syncthreads();
-    for (int o = PT / 2; o > 0; o >>= 1) {
-      if (tid < o) red[tid].x += red[tid + o].x;
-      __syncthreads();
-    }
-    if (tid == 0) part[0] = red[0];
-  } else {
-    red[tid] = dot;
-    __syncthreads();
-    if (tid < J) {
-      double2 acc = red[tid * Tj];
-      for (int q = 1; q < Tj; ++q) acc = cadd(acc, red[tid * Tj + q]);
-      part[tid] = acc;
-    }
   }
   if (!last_cta(a, b, PASS, a.nseg, &sflag)) return;
 
@@ -579,40 +621,19 @@ __global__ void k_csr_jacobi(SsCsrDev A, double2* __restrict__ out) {
 template <int DIM>
 __global__ void __launch_bounds__(PT) k_true_resid(KArgs a) {
   __shared__ double red[2][PT / 32];
-  const int b = blockIdx.x / a.nsb, sb = blockIdx.x % a.nsb;
-  if (b >= a.nb) return;
+  const int b = blockIdx.x % a.nb, sb = blockIdx.x / a.nb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double om = a.ctl[b].omega;
   const double2* x = a.X + (size_t)b * a.ld;
   const double2* rhs = a.RHS + (size_t)b * a.ld;
   double tt = 0, bb = 0;
-  const int tasks = a.kind == 0 ? a.op.nfree + a.op.npf : a.n;
-  const int t0 = (sb * (PT / 32) + warp) * SPMV_TPW;
-  for (int ti = 0; ti < SPMV_TPW; ++ti) {
-    const int task = t0 + ti;
-    if (task >= tasks) break;
-    if (a.kind == 0 && task < a.op.nfree) {
-      double2 acc[DIM];
-      saddle_vel_row<DIM>(a.op, task, om, x, lane, acc);
-      if (lane < DIM) {
-        double2 v = acc[0];
-#pragma unroll
-        for (int d = 1; d < DIM; ++d) if (lane == d) v = acc[d];
-        const double2 rb = rhs[task * DIM + lane];
-        tt += cabs2(csub(rb, v));
-        bb += cabs2(rb);
-      }
-    } else {
-      const int row = a.kind == 0 ? a.op.nfv + (task - a.op.nfree) : task;
-      const double2 v = a.kind == 0 ? saddle_pres_row<DIM>(a.op, task - a.op.nfree, x, lane)
-                                    : csr_row(a.csr, a.csr.nvals > 1 ? b : 0, task, x, lane);
-      if (lane == 0) {
-        const double2 rb = rhs[row];
-        tt += cabs2(csub(rb, v));
-        bb += cabs2(rb);
-      }
-    }
-  }
+  auto emit = [&](int row, double2 v) {
+    const double2 rb = rhs[row];
+    tt += cabs2(csub(rb, v));
+    bb += cabs2(rb);
+  };
+  if (a.kind == 0) saddle_block<DIM>(a.op, sb, om, x, emit);
+  else csr_block(a.csr, a.csr.nvals > 1 ? b : 0, sb, x, emit);
   tt = warp_sum(tt);
   bb = warp_sum(bb);
   if (lane == 0) { red[0][warp] = tt; red[1][warp] = bb; }
@@ -656,7 +677,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if (max_batch < 1) { ss_set_error("max_batch must be >= 1"); return SS_ERR_ARG; }
   KArgs& a = K->a;
   a.n = n;
-  a.ld = ss_round_up(std::max(n, 1), 32);
+  a.ld = ss_round_up(std::max(n, 1), RB);
+  a.nblk = (int)(a.ld / RB);
   a.restart = restart;
   a.jcap = restart + 1;
   a.hist_cap = std::max<int64_t>(1, hist_cap);
@@ -665,12 +687,13 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   seg = std::min<int64_t>(4096, std::max<int64_t>(256, seg));
   a.seg_rows = (int)seg;
   a.nseg = (int)((a.ld + seg - 1) / seg);
-  a.cap = 32 * a.jcap + 288;
+  a.smem_elems = PASS_SMEM_ELEMS;
   K->max_batch = max_batch;
   const size_t B = max_batch;
   int rc;
   if ((rc = kalloc(K, B * a.jcap * a.ld, &a.Q))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.W))) return rc;
+  if ((rc = kalloc(K, B * a.ld, &a.P))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.X))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.RHS))) return rc;
   if ((rc = kalloc(K, B * a.jcap, &a.qs))) return rc;
@@ -691,7 +714,7 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   SS_CUDA(cudaStreamCreateWithFlags(&K->cap_stream, cudaStreamNonBlocking));
   SS_CUDA(cudaEventCreateWithFlags(&K->ev[0], cudaEventDisableTiming));
   SS_CUDA(cudaEventCreateWithFlags(&K->ev[1], cudaEventDisableTiming));
-  K->smem_pass = (size_t)2 * a.cap * sizeof(double2);
+  K->smem_pass = (size_t)a.smem_elems * sizeof(double2);
   if (K->smem_pass + 3 * 256 * sizeof(double2) + 64 > 227 * 1024) {
     ss_set_error("restart too large for the shared-memory staging of the basis passes");
     return SS_ERR_ARG;
@@ -714,8 +737,7 @@ extern "C" int ss_krylov_create_saddle(const ss_pattern* P, int max_batch, int r
   K->device = P->device;
   K->a.kind = 0;
   K->a.op = P->op;
-  const int tasks = P->nfree + P->npf;
-  K->a.nsb = (tasks + (PT / 32) * SPMV_TPW - 1) / ((PT / 32) * SPMV_TPW);
+  K->a.nsb = saddle_nsb_host(P->nfree, P->npf);
   int rc = krylov_common_init(K, P->op.n, max_batch, restart, hist_cap);
   if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
   if (rc) { delete K; return rc; }
@@ -757,7 +779,7 @@ extern "C" int ss_krylov_create_csr(int device, int n, int64_t nnz, const int32_
     ss_count_launch();
     SS_CUDA(cudaGetLastError());
   }
-  K->a.nsb = (n + (PT / 32) * SPMV_TPW - 1) / ((PT / 32) * SPMV_TPW);
+  K->a.nsb = (n + SPMV_PROWS - 1) / SPMV_PROWS;
   rc = krylov_common_init(K, n, max_batch, restart, hist_cap);
   if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
   if (rc) { delete K; return rc; }

@@ -120,3 +120,107 @@ __device__ __forceinline__ double2 csr_row(const SsCsrDev& A, int set, int row,
   acc.y = warp_sum(acc.y);
   return acc;
 }
+
+// ------------------------------------------------------------------------------------------------
+// Block-row SpMV iterator shared by every SpMV-shaped kernel (standalone, GMRES tick, residuals).
+// A CTA of 256 threads owns a fixed block of rows of ONE mode (block -> rows never depends on the
+// batch, so per-mode reductions are batch-invariant):
+//   velocity blocks: 128 free velocity NODE rows, 8 lanes per node row (all dim components);
+//   pressure blocks: 32 pressure rows, one warp per row.
+// emit(row, value) is called by exactly one lane per output row.
+// ------------------------------------------------------------------------------------------------
+constexpr int SPMV_VROWS = 128;   // node rows per velocity block
+constexpr int SPMV_PROWS = 32;    // pressure (or generic CSR) rows per block
+
+__device__ __forceinline__ int saddle_nvb(const SsOperatorDev& op) { return (op.nfree + SPMV_VROWS - 1) / SPMV_VROWS; }
+__device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
+  return (nfree + SPMV_VROWS - 1) / SPMV_VROWS + (npf + SPMV_PROWS - 1) / SPMV_PROWS;
+}
+
+template <int DIM>
+__device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
+                                                  const double2* __restrict__ x, int gl, double2 (&acc)[DIM]) {
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
+  if (r >= 0) {
+    const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
+#pragma unroll 4
+    for (int e = e0 + gl; e < e1; e += 8) {
+      const int B = __ldg(op.ncol + e);
+      const double2 a = __ldg(op.sm + e);
+      const double am = omega * a.y;
+      const double2* xb = x + (size_t)B * DIM;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        const double2 v = xb[d];
+        acc[d].x += a.x * v.x - am * v.y;
+        acc[d].y += a.x * v.y + am * v.x;
+      }
+    }
+    const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
+#pragma unroll 2
+    for (int e = p0 + gl; e < p1; e += 8) {
+      const double2 v = x[op.nfv + __ldg(op.pcol + e)];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        const double dv = __ldg(op.dp + (size_t)e * DIM + d);
+        acc[d].x += dv * v.x;
+        acc[d].y += dv * v.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      acc[d].x += __shfl_xor_sync(0xffffffffu, acc[d].x, o);
+      acc[d].y += __shfl_xor_sync(0xffffffffu, acc[d].y, o);
+    }
+}
+
+template <int DIM, class Emit>
+__device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, double omega,
+                                             const double2* __restrict__ x, Emit&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nvb = saddle_nvb(op);
+  if (blk < nvb) {
+    const int grp = lane >> 3, gl = lane & 7;
+#pragma unroll 1
+    for (int it = 0; it < SPMV_VROWS / 32; ++it) {
+      const int r = blk * SPMV_VROWS + it * 32 + warp * 4 + grp;
+      const bool ok = r < op.nfree;
+      double2 acc[DIM];
+      saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc);
+      if (ok && gl < DIM) {
+        double2 v = acc[0];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d) if (gl == d) v = acc[d];
+        emit(r * DIM + gl, v);
+      }
+    }
+  } else {
+    const int pb = blk - nvb;
+#pragma unroll 1
+    for (int it = 0; it < SPMV_PROWS / 8; ++it) {
+      const int j = pb * SPMV_PROWS + it * 8 + warp;
+      if (j < op.npf) {
+        const double2 v = saddle_pres_row<DIM>(op, j, x, lane);
+        if (lane == 0) emit(op.nfv + j, v);
+      }
+    }
+  }
+}
+
+template <class Emit>
+__device__ __forceinline__ void csr_block(const SsCsrDev& A, int set, int blk, const double2* __restrict__ x,
+                                          Emit&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int it = 0; it < SPMV_PROWS / 8; ++it) {
+    const int row = blk * SPMV_PROWS + it * 8 + warp;
+    if (row < A.n) {
+      const double2 v = csr_row(A, set, row, x, lane);
+      if (lane == 0) emit(row, v);
+    }
+  }
+}
