@@ -414,14 +414,17 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_spmv_saddle(SsOperatorDev op, int nb, const double* __restrict__ omegas,
                                                      const double2* __restrict__ X, double2* __restrict__ Y,
                                                      int64_t ld, int jacobi) {
-  const int b = blockIdx.x % nb, blk = blockIdx.x / nb;   // mode fastest: the matrix block is shared in L2
-  const double om = omegas[b];
-  const double2* x = X + (size_t)b * ld;
-  double2* y = Y + (size_t)b * ld;
-  saddle_block<DIM>(op, blk, om, x, [&](int row, double2 v) {
-    if (jacobi && row < op.nfv) v = cmul(saddle_jacobi(op, row / DIM, om), v);
-    y[row] = v;
-  });
+  // one CTA = one row block for every mode: the block's matrix slice is re-read from L1
+  const int blk = blockIdx.x;
+  for (int b = 0; b < nb; ++b) {
+    const double om = omegas[b];
+    const double2* x = X + (size_t)b * ld;
+    double2* y = Y + (size_t)b * ld;
+    saddle_block<DIM>(op, blk, om, x, [&](int row, double2 v) {
+      if (jacobi && row < op.nfv) v = cmul(saddle_jacobi(op, row / DIM, om), v);
+      y[row] = v;
+    });
+  }
 }
 
 extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas_dev, const double* x_dev,
@@ -429,7 +432,7 @@ extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas
   if (!P || !x_dev || !y_dev || !omegas_dev || nb <= 0 || ld < P->op.n) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
   if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
   cudaStream_t st = (cudaStream_t)stream_;
-  const unsigned grid = (unsigned)(saddle_nsb_host(P->nfree, P->npf) * nb);
+  const unsigned grid = (unsigned)saddle_nsb_host(P->nfree, P->npf);
   if (P->dim == 2)
     k_spmv_saddle<2><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
   else

@@ -384,6 +384,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
         double2 p = make_double2(0.0, 0.0);
         if (cl < nr) {
           const double2* S = st + (cr + cl) * belem + lane;
+#pragma unroll 4
           for (int j = sl; j < J; j += SL) {
             const double2 q = S[j * RB], cf = coef[j];
             p.x += q.x * cf.x - q.y * cf.y;
