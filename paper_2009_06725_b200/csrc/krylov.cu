@@ -21,6 +21,7 @@
 // which other modes share the batch: per-mode results are bitwise invariant under batching and
 // mode order (the reference's test_spectral.py:187-205 contract).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <vector>
@@ -53,6 +54,7 @@ struct KArgs {
   int nseg, seg_rows;          // pass segmentation (depends on n only)
   int nsb;                     // spmv blocks per mode
   int smem_elems;              // double2 capacity of the basis-pass pipeline ring
+  int stage_div;               // a stage may use smem_elems / stage_div
   int jacobi;
   int64_t hist_cap;
   SsOperatorDev op;
@@ -345,7 +347,9 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   const int blk_end = min(blk_begin + segb, a.nblk);
   const int nblocks = blk_end - blk_begin;
   const int belem = J * RB;
-  const int CB = max(1, min(min(nblocks, 8), (a.smem_elems / 3) / (belem + RB)));
+  // passes with an update phase amortise their extra barriers over bigger chunks (measured)
+  const int div = a.stage_div > 0 ? a.stage_div : (PASS == PASS_A ? 3 : 2);
+  const int CB = max(1, min(min(nblocks, 8), (a.smem_elems / div) / (belem + RB)));
   const int stage_elems = CB * (belem + RB);
   const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
   const int nchunks = (nblocks + CB - 1) / CB;
@@ -514,27 +518,40 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     }
     return;
   }
-  // PASS_C: Givens update (krylov.py:115-149), single thread for the serial recurrence.
+  // PASS_C: Givens update (krylov.py:115-149).  The H column and the stored rotations are staged
+  // in (now idle) shared memory by all threads; one thread runs the serial recurrence on them.
   __shared__ double2 y[256];
   __shared__ int s_solve;
+  const int jc = a.jcap;
+  double2* hs = smem;               // column k (k+2 entries)
+  double2* css = smem + 256;        // cs[0..k)
+  double2* sns = smem + 512;        // sn[0..k)
+  {
+    const double2* c1 = a.C1 + (size_t)b * jc;
+    const double2* c2 = a.C2 + (size_t)b * jc;
+    const double2* csg = a.CS + (size_t)b * a.restart;
+    const double2* sng = a.SN + (size_t)b * a.restart;
+    for (int i = tid; i <= k; i += PT) {
+      hs[i] = cadd(c1[i], c2[i]);
+      if (i < k) { css[i] = csg[i]; sns[i] = sng[i]; }
+    }
+  }
+  __syncthreads();
   if (tid == 0) {
     double nsq = 0;
     for (int q = 0; q < SL; ++q) nsq += red[q].x;
     const double hk = sqrt(nsq);
-    const int jc = a.jcap;
-    double2* h = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
-    const double2* c1 = a.C1 + (size_t)b * jc;
-    const double2* c2 = a.C2 + (size_t)b * jc;
-    for (int i = 0; i <= k; ++i) h[i] = cadd(c1[i], c2[i]);
+    double2* h = hs;
     double2* cs = a.CS + (size_t)b * a.restart;
     double2* sn = a.SN + (size_t)b * a.restart;
     double2* g = a.G + (size_t)b * jc;
+    double2 hi = h[0];
     for (int i = 0; i < k; ++i) {
-      const double2 hi = h[i], hi1 = h[i + 1];
-      const double2 tmp = cadd(cmul(cs[i], hi), cmul(sn[i], hi1));
-      h[i + 1] = cadd(cmul(make_double2(-sn[i].x, sn[i].y), hi), cmul(conjd(cs[i]), hi1));
-      h[i] = tmp;
+      const double2 hi1 = h[i + 1], ci = css[i], si = sns[i];
+      h[i] = cadd(cmul(ci, hi), cmul(si, hi1));
+      hi = cadd(cmul(make_double2(-si.x, si.y), hi), cmul(conjd(ci), hi1));
     }
+    h[k] = hi;
     const double ahkk = hypot(h[k].x, h[k].y);
     const double denom = sqrt(ahkk * ahkk + hk * hk);
     int exit_cycle = 0;
@@ -548,7 +565,6 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
       cs[k] = csk;
       sn[k] = snk;
       h[k] = cadd(cmul(csk, h[k]), cscale(snk, hk));
-      h[k + 1] = make_double2(0.0, 0.0);
       const double2 gk = g[k];
       g[k + 1] = cmul(make_double2(-snk.x, snk.y), gk);
       g[k] = cmul(csk, gk);
@@ -567,6 +583,8 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
         if (est <= c->target || c->k >= a.restart || c->iters >= c->maxiter) exit_cycle = 1;
       }
     }
+    h[k + 1] = make_double2(hk, 0.0);
+    if (denom != 0.0) h[k + 1] = make_double2(0.0, 0.0);
     s_solve = 0;
     if (exit_cycle) {
       const int kk = c->k;
@@ -579,10 +597,14 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     }
   }
   __syncthreads();
+  {
+    double2* hg = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
+    for (int i = tid; i <= k + 1; i += PT) hg[i] = hs[i];
+  }
+  __syncthreads();
   const int kk = s_solve;
   if (kk == 0) return;
   // Cycle end: y = H[:k,:k]^-1 g[:k] (column-oriented back substitution, krylov.py:151-153,167-168)
-  const int jc = a.jcap;
   const double2* hb = a.H + (size_t)b * a.restart * jc;
   const double2* g = a.G + (size_t)b * jc;
   for (int i = tid; i < kk; i += PT) y[i] = g[i];
@@ -689,6 +711,9 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   a.seg_rows = (int)seg;
   a.nseg = (int)((a.ld + seg - 1) / seg);
   a.smem_elems = PASS_SMEM_ELEMS;
+  a.stage_div = 0;   // 0 = per-pass default
+  if (const char* e = getenv("SS_PASS_SMEM")) a.smem_elems = std::max(2048, std::min(PASS_SMEM_ELEMS, atoi(e)));
+  if (const char* e = getenv("SS_PASS_DIV")) a.stage_div = std::max(1, atoi(e));
   K->max_batch = max_batch;
   const size_t B = max_batch;
   int rc;
