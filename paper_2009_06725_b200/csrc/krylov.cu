@@ -61,7 +61,9 @@ struct KArgs {
   SsCsrDev csr;
   ModeCtl* ctl;
   double2 *Q, *W, *X, *RHS;
-  double2* P;                  // current raw basis vector q_k in row layout (SpMV input)
+  double2* P;                  // current raw basis vectors, mode-interleaved [row][pstride] (SpMV input)
+  int pstride;                 // = max batch
+  int spmv_split;              // sub-CTAs per SpMV row block (fills the GPU when n is small)
   int nblk;                    // ld / RB row blocks; Q is row-block-major: [b][blk][jcap][RB]
   double* qs;                  // [b][jcap] scale of raw basis vectors
   double2 *H, *G, *CS, *SN, *C1, *C2, *Y;
@@ -177,56 +179,161 @@ __global__ void __launch_bounds__(PT) k_init(KArgs a) {
 
 // ------------------------------------------------------------------------------------------------
 // Tick kernel 1: SpMV (inner w = s.(A q_k)) or residual (t = b - A x, r = s.t) + cycle decisions.
+//
+// The current raw basis vectors of all modes live in P with a MODE-INTERLEAVED layout
+// P[row * pstride + mode]: one gather of node B's component d returns that value for every mode
+// of the batch as one contiguous run, so a warp whose lanes are modes issues coalesced gathers
+// and shares every matrix-entry load (broadcast) across the batch.  Each lane owns one
+// (row, mode) pair and sums the row's entries sequentially: no cross-lane reduction, and a
+// mode's result never depends on the other modes in the batch.
 // ------------------------------------------------------------------------------------------------
+constexpr int MAXB_SMEM = 256;   // modes whose per-tick state is cached in shared memory
+
 template <int DIM>
-__global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
-  __shared__ double red[2][PT / 32];
-  __shared__ int sflag;
-  const int b = blockIdx.x % a.nb, sb = blockIdx.x / a.nb;   // mode fastest: one row block's CTAs co-run
-  ModeCtl* c = a.ctl + b;
-  const int phase = c->phase;
-  if (phase != PH_INNER && phase != PH_START && phase != PH_RESID) return;
-  const bool resid = phase == PH_RESID;
+__device__ __forceinline__ void spmv_inner_interleaved(const KArgs& a, int blk, const int* sph,
+                                                       const double* som, const double* sxs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double om = c->omega;
-  const int k = c->k;
-  const double2* x = (resid ? a.X : a.P) + (size_t)b * a.ld;
-  const double xs = resid ? 1.0 : a.qs[b * a.jcap + k];
-  double2* out = resid ? a.P + (size_t)b * a.ld : a.W + (size_t)b * a.ld;
+  const int MP = a.nb >= 32 ? 32 : (a.nb > 16 ? 32 : a.nb > 8 ? 16 : a.nb > 4 ? 8 : a.nb > 2 ? 4 : a.nb > 1 ? 2 : 1);
+  const int RPW = 32 / MP;            // rows per warp
+  const int rs = lane / MP, ml = lane % MP;
+  const int sub = blockIdx.x % a.spmv_split;             // sub-CTAs sharing one row block
+  const int slot0 = sub * 8 * RPW + warp * RPW + rs;      // row slot of this lane within the block
+  const int sstep = a.spmv_split * 8 * RPW;
+  const SsOperatorDev& op = a.op;
+  const int ps = a.pstride;
+  const int nvb = saddle_nvb(op);
+  for (int mg = 0; mg < a.nb; mg += MP) {
+    const int m = mg + ml;
+    bool act = m < a.nb;
+    const int ph = act ? sph[m] : PH_IDLE;
+    act = act && (ph == PH_INNER || ph == PH_START);
+    const double om = act ? som[m] : 0.0;
+    const double xs = act ? sxs[m] : 0.0;
+    double2* w = a.W + (size_t)(act ? m : 0) * a.ld;
+    const double2* P = a.P + m;       // column m of the interleaved array
+    if (blk < nvb) {
+      for (int r = blk * SPMV_VROWS + slot0; r < min((blk + 1) * SPMV_VROWS, op.nfree); r += sstep) {
+        if (!act) continue;
+        double2 acc[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
+        const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
+#pragma unroll 4
+        for (int e = e0; e < e1; ++e) {
+          const int B = __ldg(op.ncol + e);
+          const double2 sm = __ldg(op.sm + e);
+          const double am = om * sm.y;
+          const double2* xb = P + (size_t)B * DIM * ps;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double2 v = xb[(size_t)d * ps];
+            acc[d].x += sm.x * v.x - am * v.y;
+            acc[d].y += sm.x * v.y + am * v.x;
+          }
+        }
+        const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
+#pragma unroll 2
+        for (int e = p0; e < p1; ++e) {
+          const double2 v = P[(size_t)(op.nfv + __ldg(op.pcol + e)) * ps];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double dv = __ldg(op.dp + (size_t)e * DIM + d);
+            acc[d].x += dv * v.x;
+            acc[d].y += dv * v.y;
+          }
+        }
+        const double2 sj = a.jacobi ? saddle_jacobi(op, r, om) : make_double2(1.0, 0.0);
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) w[r * DIM + d] = cmul(sj, cscale(acc[d], xs));
+      }
+    } else {
+      const int pb = blk - nvb;
+      for (int j = pb * SPMV_PROWS + slot0; j < min((pb + 1) * SPMV_PROWS, op.npf); j += sstep) {
+        if (!act) continue;
+        double2 acc = make_double2(0.0, 0.0);
+        const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
+#pragma unroll 4
+        for (int e = e0; e < e1; ++e) {
+          const double2* xb = P + (size_t)__ldg(op.tcol + e) * DIM * ps;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double dv = __ldg(op.dt + (size_t)e * DIM + d);
+            const double2 v = xb[(size_t)d * ps];
+            acc.x += dv * v.x;
+            acc.y += dv * v.y;
+          }
+        }
+        w[op.nfv + j] = cscale(acc, xs);
+      }
+    }
+  }
+}
+
+// RESID for one mode (row layout X): t = b - A x, r = s.t -> P (interleaved) and Q[0]; norms.
+template <int DIM>
+__device__ __forceinline__ void spmv_resid_mode(const KArgs& a, int b, int sb, double om) {
+  __shared__ double red[2][PT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double2* x = a.X + (size_t)b * a.ld;
   const double2* rhs = a.RHS + (size_t)b * a.ld;
   double tt = 0, rr = 0;
   auto emit = [&](int row, double2 v) {
     const double2 s = row_scale<DIM>(a, b, row, om);
-    if (resid) {
-      const double2 t = csub(rhs[row], v);
-      const double2 r = cmul(s, t);
-      out[row] = r;
-      qat(a, b, 0, row) = r;
-      tt += cabs2(t);
-      rr += cabs2(r);
-    } else {
-      out[row] = cmul(s, cscale(v, xs));
-    }
+    const double2 t = csub(rhs[row], v);
+    const double2 r = cmul(s, t);
+    a.P[(size_t)row * a.pstride + b] = r;
+    qat(a, b, 0, row) = r;
+    tt += cabs2(t);
+    rr += cabs2(r);
   };
   if (a.kind == 0) saddle_block<DIM>(a.op, sb, om, x, emit);
   else csr_block(a.csr, a.csr.nvals > 1 ? b : 0, sb, x, emit);
-  if (resid) {
-    tt = warp_sum(tt);
-    rr = warp_sum(rr);
-    if (lane == 0) { red[0][warp] = tt; red[1][warp] = rr; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s0 = 0, s1 = 0;
-      for (int w = 0; w < PT / 32; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
-      a.spart[(size_t)b * a.nsb + sb] = make_double2(s0, s1);
+  tt = warp_sum(tt);
+  rr = warp_sum(rr);
+  if (lane == 0) { red[0][warp] = tt; red[1][warp] = rr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0, s1 = 0;
+    for (int w = 0; w < PT / 32; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
+    a.spart[(size_t)b * a.nsb + sb] = make_double2(s0, s1);
+  }
+  __syncthreads();
+}
+
+// Generic-CSR inner SpMV for one mode (row layout through P column b).
+__device__ __forceinline__ void spmv_inner_csr_mode(const KArgs& a, int b, int sb, double xs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SsCsrDev& A = a.csr;
+  const int set = A.nvals > 1 ? b : 0;
+  const double2* vals = A.vals + (size_t)set * A.nnz;
+  for (int it = 0; it < SPMV_PROWS / 8; ++it) {
+    const int row = sb * SPMV_PROWS + it * 8 + warp;
+    if (row >= A.n) break;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e = A.indptr[row] + lane; e < A.indptr[row + 1]; e += 32) {
+      const double2 av = vals[e];
+      const double2 v = a.P[(size_t)A.indices[e] * a.pstride + b];
+      acc.x += av.x * v.x - av.y * v.y;
+      acc.y += av.x * v.y + av.y * v.x;
+    }
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    if (lane == 0) {
+      const double2 s = A.scale && a.jacobi ? A.scale[(size_t)set * A.n + row] : make_double2(1.0, 0.0);
+      a.W[(size_t)b * a.ld + row] = cmul(s, cscale(acc, xs));
     }
   }
-  if (!last_cta(a, b, 0, a.nsb, &sflag)) return;
-  if (!resid) {
+}
+
+// Cycle-boundary decisions of mode b once every CTA has contributed (krylov.py:93-103,155-162).
+__device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int phase, int* sflag) {
+  if (!last_cta(a, b, 0, a.nsb * a.spmv_split, sflag)) return;
+  ModeCtl* c = a.ctl + b;
+  if (phase != PH_RESID) {
     if (threadIdx.x == 0 && phase == PH_START) c->phase = PH_INNER;
+    __syncthreads();
     return;
   }
-  // Residual reduction (fixed order) and the cycle-boundary decisions (krylov.py:93-103,155-162).
   __shared__ double2 rsum[PT];
   double2 acc = make_double2(0.0, 0.0);
   for (int q = threadIdx.x; q < a.nsb; q += PT) {
@@ -268,6 +375,43 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   if (c->phase == PH_START) {
     double2* g = a.G + (size_t)b * a.jcap;
     for (int j = threadIdx.x; j < a.jcap; j += PT) g[j] = make_double2(j == 0 ? c->beta : 0.0, 0.0);
+  }
+  __syncthreads();
+}
+
+// One CTA = one row block, all modes of the batch.
+template <int DIM>
+__global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
+  __shared__ int sph[MAXB_SMEM];
+  __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
+  __shared__ int sflag, s_any_inner;
+  const int sb = blockIdx.x / a.spmv_split, sub = blockIdx.x % a.spmv_split;
+  if (threadIdx.x == 0) s_any_inner = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.nb; b += PT) {
+    const ModeCtl* c = a.ctl + b;
+    const int ph = c->phase;
+    sph[b] = ph;
+    som[b] = c->omega;
+    sxs[b] = (ph == PH_INNER || ph == PH_START) ? a.qs[b * a.jcap + c->k] : 0.0;
+    if (ph == PH_INNER || ph == PH_START) s_any_inner = 1;
+  }
+  __syncthreads();
+  if (s_any_inner) {
+    if (a.kind == 0) {
+      spmv_inner_interleaved<DIM>(a, sb, sph, som, sxs);
+    } else {
+      if (sub == 0)
+        for (int b = 0; b < a.nb; ++b)
+          if (sph[b] == PH_INNER || sph[b] == PH_START) spmv_inner_csr_mode(a, b, sb, sxs[b]);
+    }
+  }
+  if (sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
+    for (int b = 0; b < a.nb; ++b)
+      if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
+  for (int b = 0; b < a.nb; ++b) {
+    const int ph = sph[b];
+    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph, &sflag);
   }
 }
 
@@ -406,7 +550,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
           const int64_t row = (int64_t)(c0 + c) * RB + lane;
           if (PASS == PASS_C) {
             qblock(a, b, c0 + c)[(size_t)(k + 1) * RB + lane] = v;   // raw q_{k+1}
-            a.P[(size_t)b * a.ld + row] = v;
+            a.P[(size_t)row * a.pstride + b] = v;
             nrm += cabs2(v);
           } else {
             vec[row] = v;
@@ -697,7 +841,7 @@ static int kalloc(ss_krylov* K, size_t count, T** p) {
 
 static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, int64_t hist_cap) {
   if (restart < 1 || restart > 240) { ss_set_error("restart must lie in [1, 240]"); return SS_ERR_ARG; }
-  if (max_batch < 1) { ss_set_error("max_batch must be >= 1"); return SS_ERR_ARG; }
+  if (max_batch < 1 || max_batch > MAXB_SMEM) { ss_set_error("max_batch must lie in [1, 256]"); return SS_ERR_ARG; }
   KArgs& a = K->a;
   a.n = n;
   a.ld = ss_round_up(std::max(n, 1), RB);
@@ -720,6 +864,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if ((rc = kalloc(K, B * a.jcap * a.ld, &a.Q))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.W))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.P))) return rc;
+  a.pstride = max_batch;
+  if (a.spmv_split < 1) a.spmv_split = 1;   // the saddle creator sets it from nsb
   if ((rc = kalloc(K, B * a.ld, &a.X))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.RHS))) return rc;
   if ((rc = kalloc(K, B * a.jcap, &a.qs))) return rc;
@@ -764,6 +910,7 @@ extern "C" int ss_krylov_create_saddle(const ss_pattern* P, int max_batch, int r
   K->a.kind = 0;
   K->a.op = P->op;
   K->a.nsb = saddle_nsb_host(P->nfree, P->npf);
+  K->a.spmv_split = std::max(1, std::min(16, (8 * 148 + K->a.nsb - 1) / K->a.nsb));
   int rc = krylov_common_init(K, P->op.n, max_batch, restart, hist_cap);
   if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
   if (rc) { delete K; return rc; }
@@ -844,7 +991,7 @@ extern "C" int ss_krylov_buffers(ss_krylov* K, double** rhs, double** x, int64_t
 template <int DIM>
 static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
   const unsigned gs = (unsigned)(a.nb * a.nseg);
-  k_tick_spmv<DIM><<<a.nb * a.nsb, PT, 0, st>>>(a);
+  k_tick_spmv<DIM><<<a.nsb * a.spmv_split, PT, 0, st>>>(a);
   SS_LAUNCH_CHECK();
   k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
   SS_LAUNCH_CHECK();
@@ -1094,7 +1241,7 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
   int done = 0;
   while (tick < max_ticks) {
     SS_CUDA(cudaEventRecord(ev[0], st));
-    k_tick_spmv<DIM><<<a.nb * a.nsb, PT, 0, st>>>(a);
+    k_tick_spmv<DIM><<<a.nsb * a.spmv_split, PT, 0, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[1], st));
     k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
