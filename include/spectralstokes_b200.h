@@ -52,6 +52,10 @@ int ss_pattern_info(const ss_pattern* p, int64_t* info);
 /* Bit-exact reduced CSR pattern (= ComplexSaddleSystem.matrix.indptr/.indices, assembly.py:479).
  * indices may be NULL to obtain indptr only. */
 int ss_pattern_export(const ss_pattern* p, int32_t* indptr_host, int32_t* indices_host);
+/* Columns of selected rows of the same reduced CSR (sampled parity checks on very large meshes).
+ * counts[i] receives the nnz of rows[i]; indices (capacity cap, may be NULL) the concatenated columns. */
+int ss_pattern_export_rows(const ss_pattern* p, int64_t nrows, const int64_t* rows_host, int64_t* counts_host,
+                           int32_t* indices_host, int64_t cap);
 /* ComplexSaddleSystem.vel_dof (n_vel_nodes x dim) and .pres_dof (n_vertices) (assembly.py:319-320). */
 int ss_pattern_dof_maps(const ss_pattern* p, int64_t* vel_dof_host, int64_t* pres_dof_host);
 

@@ -24,6 +24,7 @@ from .scvs import (  # noqa: F401
     mode_coefficients,
     reconstruct,
     reference_tables,
+    sampled_rows,
     solve_mode,
     surface_load,
 )

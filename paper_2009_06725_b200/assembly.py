@@ -223,6 +223,17 @@ class SaddleOperator:
             self._pattern = (ip, ix)
         return self._pattern
 
+    def pattern_rows(self, rows):
+        """Column indices of selected reduced rows (list of int32 arrays), bit-exact like pattern()."""
+        rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+        counts = np.zeros(rows.size, dtype=np.int64)
+        _lib.call("ss_pattern_export_rows", self._h, rows.size, _lib.ptr(rows, C.c_int64), _lib.ptr(counts, C.c_int64),
+                  None, 0)
+        idx = np.zeros(max(1, int(counts.sum())), dtype=np.int32)
+        _lib.call("ss_pattern_export_rows", self._h, rows.size, _lib.ptr(rows, C.c_int64), _lib.ptr(counts, C.c_int64),
+                  _lib.ptr(idx, C.c_int32), idx.size)
+        return np.split(idx[: int(counts.sum())], np.cumsum(counts)[:-1])
+
     def dof_maps(self):
         if self._dof is None:
             vd = np.zeros((self.n_vel_nodes, self.dim), dtype=np.int64)

@@ -449,3 +449,37 @@ extern "C" int ss_surface_load(int dim, int64_t nvn, const double* nodes, int64_
   }
   return SS_OK;
 }
+
+// Column indices of selected rows of the reduced vector CSR (same order as ss_pattern_export), for
+// sampled parity checks on meshes too large to export whole.  counts[i] = nnz of rows[i];
+// indices receives the concatenated columns (capacity cap); returns SS_ERR_ARG if cap is short.
+extern "C" int ss_pattern_export_rows(const ss_pattern* P, int64_t nrows, const int64_t* rows, int64_t* counts,
+                                      int32_t* indices, int64_t cap) {
+  if (!P || (nrows > 0 && (!rows || !counts))) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  const int dim = P->dim, nfv = P->nfree * dim;
+  int64_t pos = 0;
+  for (int64_t i = 0; i < nrows; ++i) {
+    const int64_t row = rows[i];
+    if (row < 0 || row >= (int64_t)nfv + P->npf) { ss_set_error("row out of range"); return SS_ERR_ARG; }
+    int64_t c = 0;
+    if (row < nfv) {
+      const int r = (int)(row / dim), d = (int)(row % dim);
+      c = (P->nptr[r + 1] - P->nptr[r]) + (P->pptr[r + 1] - P->pptr[r]);
+      if (indices) {
+        if (pos + c > cap) { ss_set_error("index buffer too small"); return SS_ERR_ARG; }
+        for (int e = P->nptr[r]; e < P->nptr[r + 1]; ++e) indices[pos++] = P->ncol[e] * dim + d;
+        for (int e = P->pptr[r]; e < P->pptr[r + 1]; ++e) indices[pos++] = nfv + P->pcol[e];
+      }
+    } else {
+      const int j = (int)(row - nfv);
+      c = (int64_t)dim * (P->tptr[j + 1] - P->tptr[j]);
+      if (indices) {
+        if (pos + c > cap) { ss_set_error("index buffer too small"); return SS_ERR_ARG; }
+        for (int e = P->tptr[j]; e < P->tptr[j + 1]; ++e)
+          for (int dd = 0; dd < dim; ++dd) indices[pos++] = P->tcol[e] * dim + dd;
+      }
+    }
+    counts[i] = c;
+  }
+  return SS_OK;
+}

@@ -118,7 +118,7 @@ class KrylovWorkspace:
         nb = om.size
         if nb > self.max_batch:
             raise ValueError("batch larger than the workspace")
-        x = x_out if x_out is not None else torch.empty((nb, self.ld), dtype=torch.complex128, device=self.device)
+        x = x_out if x_out is not None else torch.zeros((nb, self.ld), dtype=torch.complex128, device=self.device)
         if x0 is not None and x0.data_ptr() != x.data_ptr():
             x.copy_(x0)
         oi = np.zeros(6 * nb, dtype=np.int64)

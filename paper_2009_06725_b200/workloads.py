@@ -17,6 +17,7 @@ import numpy as np
 
 from .mesh import Mesh, promote_to_quadratic, with_patch_kinds
 from .structured import channel_grid, jittered_pipe, parabolic_inlet_profile, pipe_grid
+from .vessels import bent_pipe, y_junction
 
 C1_TOL = 1e-10
 
@@ -99,3 +100,37 @@ def pipe3d_case() -> Case:
     mesh = with_patch_kinds(m, {"inlet": "dirichlet"})
     return Case("pipe3d_3x15", mesh, geom, 1.06, 0.04, 1.0, 16,
                 _coefficients(2, 16, lambda n: 1.0 + n ** 1.5), "inlet", "dirichlet", radius=0.5)
+
+
+def c3_case(n_rings: int = 20) -> Case:
+    """Config 3: 90-degree bend (bend radius 2, R = 0.5), ~2.06 M tets at n_rings = 20, 64 modes ~ 1/n^2."""
+    mesh = bent_pipe(n_rings, 0.5, 2.0, 2.0)
+    return Case(f"c3_bend_{mesh.n_elements}tets", mesh, None, 1.06, 0.04, 1.0, 63,
+                _coefficients(3, 63, lambda n: n.astype(float) ** 2), "inlet", "dirichlet", radius=0.5)
+
+
+def c4_case(n_rings: int = 27) -> Case:
+    """Config 4: seeded Y-junction, ~4.96 M tets at n_rings = 27, 32 modes, two zero-traction outlets."""
+    mesh, _ = y_junction(n_rings, seed=104)
+    return Case(f"c4_yjunction_{mesh.n_elements}tets", mesh, None, 1.06, 0.04, 1.0, 31,
+                _coefficients(4, 31, lambda n: 1.0 + n ** 1.5), "inlet", "dirichlet", radius=0.5)
+
+
+def c5_case(n_rings: int = 35, n_layers: int = 363) -> Case:
+    """Config 5: jittered straight pipe, ~8.0 M tets at (35, 363), 128 modes ~ N(0,1)/(1+n^2)."""
+    mesh, geom = jittered_pipe(n_rings, n_layers, 0.5, 5.0, seed=105)
+    return Case(f"c5_pipe_{mesh.n_elements}tets", mesh, geom, 1.06, 0.04, 1.0, 127,
+                _coefficients(5, 127, lambda n: 1.0 + n ** 2), "inlet", "dirichlet", radius=0.5)
+
+
+# Down-scaled instances of the SAME generators (CPU-convergeable; parity at 1e-10 vs the reference)
+def c3_small() -> Case:
+    return c3_case(2)
+
+
+def c4_small() -> Case:
+    return c4_case(2)
+
+
+def c5_small() -> Case:
+    return c5_case(3, 12)

@@ -17,6 +17,8 @@ Fixtures
                                                                                  spectral.py:254-317)
   pipe3d.npz      down-scaled 3D pipe (pipe_grid(3,15)), parabolic Dirichlet inlet, modes 1 and 16
   c2_pattern.npz  BASELINE config 2 (jittered 199 800-tet pipe): pattern hash, sampled A@x and rhs
+  small3d.npz     down-scaled instances of the config 3/4/5 generators (bend, Y-junction, jittered
+                  pipe), two modes each solved by the reference to 1e-10
 """
 
 from __future__ import annotations
@@ -48,7 +50,7 @@ from spectralstokes import spectral as RSP  # noqa: E402
 from spectralstokes import structured as RS  # noqa: E402
 
 from paper_2009_06725_b200.workloads import (  # noqa: E402
-    C1_TOL, c1_case, c2_case, pipe3d_case,
+    C1_TOL, c1_case, c2_case, c3_small, c4_small, c5_small, pipe3d_case,
 )
 
 
@@ -196,6 +198,38 @@ def make_pipe3d(pool):
     print("pipe3d iterations", [(r[0], r[3]) for r in res])
 
 
+# -- down-scaled configs 3, 4, 5 -----------------------------------------------------------------
+
+SMALL = {"c3": (c3_small, [1, 8]), "c4": (c4_small, [1, 8]), "c5": (c5_small, [1, 16])}
+
+
+def _small_solve(args):
+    tag, idx = args
+    case = SMALL[tag][0]()
+    geom = "cylinder" if case.geometry is not None else None
+    q = _ref_qmesh(case.mesh, geom, case.radius)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    s = RA.assemble_mode_system(q, props, float(case.omegas[idx]), g_mode=case.coefficients[idx] * case.profile)
+    t0 = time.perf_counter()
+    x, rep = RK.gmres_solve(s, RK.SolverSettings(tolerance=C1_TOL, restart=200))
+    u, p = s.expand(x)
+    return (tag, idx, u, p, rep.iterations, rep.residual, rep.converged, time.perf_counter() - t0, s.rhs,
+            _sha(s.matrix.indptr, s.matrix.indices), s.matrix.nnz, _sha(q.nodes), _sha(q.vel_conn))
+
+
+def make_small3d(pool):
+    jobs = [(tag, i) for tag, (_, idxs) in SMALL.items() for i in idxs]
+    out = {}
+    for tag, idx, u, p, it, r, conv, wall, rhs, psha, nnz, nsha, csha in pool.map(_small_solve, jobs):
+        k = f"{tag}_{idx}"
+        out[f"{k}_u"], out[f"{k}_p"], out[f"{k}_rhs"] = u, p, rhs
+        out[f"{k}_iters"], out[f"{k}_res"], out[f"{k}_conv"], out[f"{k}_wall"] = it, r, conv, wall
+        out[f"{k}_pattern_sha"], out[f"{k}_nnz"] = np.array(psha), np.int64(nnz)
+        out[f"{tag}_nodes_sha"], out[f"{tag}_conn_sha"] = np.array(nsha), np.array(csha)
+        print(k, it, r, conv, round(wall, 1))
+    np.savez_compressed(HERE / "small3d.npz", **out)
+
+
 # -- config 2 pattern --------------------------------------------------------------------------------
 
 def make_c2_pattern():
@@ -224,7 +258,7 @@ def make_c2_pattern():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d"]
+    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d"]
     with Pool(min(9, os.cpu_count() or 1)) as pool:
         if "shapes" in what:
             make_shapes()
@@ -236,3 +270,5 @@ if __name__ == "__main__":
             make_c1(pool)
         if "pipe3d" in what:
             make_pipe3d(pool)
+        if "small3d" in what:
+            make_small3d(pool)
