@@ -662,10 +662,25 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   const int JR = PASS == PASS_C ? 1 : J;
   const int SL = max(1, PT / JR);      // slices over segments
   {
+    // 8 independent accumulators keep 8 L2 loads in flight per thread; combined in fixed order
     const int j = tid % JR, sl = tid / JR;
-    double2 acc = make_double2(0.0, 0.0);
-    if (sl < SL)
-      for (int q = sl; q < a.nseg; q += SL) acc = cadd(acc, __ldcg(pb + (size_t)q * a.jcap + j));
+    double2 acc8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc8[u] = make_double2(0.0, 0.0);
+    if (sl < SL) {
+      int q = sl;
+      for (; q + 7 * SL < a.nseg; q += 8 * SL) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(pb + (size_t)(q + u * SL) * a.jcap + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc8[u] = cadd(acc8[u], v[u]);
+      }
+      for (int u = 0; q < a.nseg; q += SL, ++u) acc8[u] = cadd(acc8[u], __ldcg(pb + (size_t)q * a.jcap + j));
+    }
+    double2 acc = acc8[0];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) acc = cadd(acc, acc8[u]);
     red[tid] = acc;
   }
   __syncthreads();
