@@ -88,6 +88,9 @@ int64_t ss_spmv_bytes(const ss_pattern* p, int nb);
  * assembly.py:357-362).  out_host: nb doubles. */
 int ss_residual_norms(const ss_pattern* p, int nb, const double* omegas_dev, const double* rhs_dev, const double* x_dev,
                       int64_t ld, double* out_host, void* stream);
+/* L2(Omega) norms of nb nodal velocity-space fields (nb x n_vel_nodes x ncomp complex) by element
+ * quadrature (metrics.l2_norm, metrics.py:12-18; interpolate_at_quadrature, assembly.py:497-511). */
+int ss_l2_norms(const ss_pattern* p, int nb, int ncomp, const double* fields_dev, double* out_host, void* stream);
 /* Jacobi scale vectors 1/diag (1 where diag = 0) per mode (jacobi_precondition, krylov.py:49-60). */
 int ss_jacobi(const ss_pattern* p, int nb, const double* omegas_dev, double* scale_dev, int64_t ld, void* stream);
 /* Reduced solutions -> nodal velocity (nb x n_vel_nodes*dim) and pressure (nb x n_vertices),

@@ -21,6 +21,7 @@ from .scvs import (  # noqa: F401
     gmres_inner_step_cost,
     gmres_solve,
     jacobi_scale,
+    l2_norm,
     mode_coefficients,
     reconstruct,
     reference_tables,

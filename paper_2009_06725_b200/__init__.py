@@ -28,8 +28,11 @@ from .mesh import (  # noqa: F401
     QuadraticMesh,
     promote_to_quadratic,
 )
+from .metrics import l2_norm, l2_norms  # noqa: F401
 from .spectral import (  # noqa: F401
     BoundaryWaveform,
+    adaptive_mode_refinement,
+    mode_energies,
     ModeSet,
     ModeSolution,
     fourier_transform_bcs,

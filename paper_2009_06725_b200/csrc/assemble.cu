@@ -507,3 +507,140 @@ extern "C" int ss_residual_norms(const ss_pattern* P, int nb, const double* omeg
   }
   return SS_OK;
 }
+
+// ------------------------------------------------------------------------------------------------
+// Mode-batched L2(Omega) norms of nodal velocity-space fields (metrics.l2_norm, reference
+// metrics.py:12-18 with interpolate_at_quadrature, assembly.py:497-511): per element |det J|, the
+// field at the degree-4 quadrature points, w_q |u_q|^2 summed over components.  Per-CTA partials,
+// summed on the host in fixed order (deterministic).  fields: [b][nvn][ncomp] complex.
+// ------------------------------------------------------------------------------------------------
+__constant__ double c_qw[16];          // quadrature weights
+__constant__ double c_phi[16 * 10];    // P2 values at the quadrature points [q][a]
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_l2_partials(const int* __restrict__ conn, const double* __restrict__ vnodes,
+                                                     int64_t ne, int64_t nvn, int ncomp, int nq,
+                                                     const double2* __restrict__ fields, double* __restrict__ part) {
+  constexpr int NL = DIM == 2 ? 6 : 10, NV = DIM + 1;
+  __shared__ double red[256];
+  const int b = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  if (e < ne) {
+    const int* c = conn + e * NL;
+    double x[NV][DIM];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) x[v][d] = vnodes[(size_t)c[v] * DIM + d];
+    double det;
+    if (DIM == 2) {
+      det = (x[1][0] - x[0][0]) * (x[2][1] - x[0][1]) - (x[2][0] - x[0][0]) * (x[1][1] - x[0][1]);
+    } else {
+      const double a0 = x[1][0] - x[0][0], a1 = x[1][1] - x[0][1], a2 = x[1][2] - x[0][2];
+      const double b0 = x[2][0] - x[0][0], b1 = x[2][1] - x[0][1], b2 = x[2][2] - x[0][2];
+      const double c0 = x[3][0] - x[0][0], c1 = x[3][1] - x[0][1], c2 = x[3][2] - x[0][2];
+      det = a0 * (b1 * c2 - b2 * c1) - b0 * (a1 * c2 - a2 * c1) + c0 * (a1 * b2 - a2 * b1);
+    }
+    const double2* f = fields + (size_t)b * nvn * ncomp;
+    for (int comp = 0; comp < ncomp; ++comp) {
+      double2 u[NL];
+#pragma unroll
+      for (int a = 0; a < NL; ++a) u[a] = f[(size_t)c[a] * ncomp + comp];
+      for (int q = 0; q < nq; ++q) {
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < NL; ++a) {
+          v.x += c_phi[q * NL + a] * u[a].x;
+          v.y += c_phi[q * NL + a] * u[a].y;
+        }
+        acc += c_qw[q] * (v.x * v.x + v.y * v.y);
+      }
+    }
+    acc *= fabs(det);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(size_t)b * gridDim.x + blockIdx.x] = red[0];
+}
+
+extern "C" int ss_l2_norms(const ss_pattern* P, int nb, int ncomp, const double* fields_dev, double* out_host,
+                           void* stream_) {
+  if (!P || nb < 1 || ncomp < 1 || !fields_dev || !out_host) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  // degree-4 rule and P2 values at its points (same construction as reference_tables)
+  const int dim = P->dim, nl = dim == 2 ? 6 : 10;
+  std::vector<std::vector<double>> bary;
+  std::vector<double> w;
+  if (dim == 2) {
+    const double A[2] = {0.445948490915965, 0.091576213509771};
+    const double W[2] = {0.223381589678011, 0.109951743655322};
+    for (int g = 0; g < 2; ++g)
+      for (int i = 0; i < 3; ++i) {
+        std::vector<double> bb(3, A[g]);
+        bb[i] = 1 - 2 * A[g];
+        bary.push_back(bb);
+        w.push_back(0.5 * W[g]);
+      }
+  } else {
+    const double s = std::sqrt(5.0 / 14.0), hi = (1.0 + s) / 4.0, lo = (1.0 - s) / 4.0;
+    bary.push_back({0.25, 0.25, 0.25, 0.25});
+    w.push_back(-74.0 / 5625.0);
+    for (int i = 0; i < 4; ++i) {
+      std::vector<double> bb(4, 1.0 / 14.0);
+      bb[i] = 11.0 / 14.0;
+      bary.push_back(bb);
+      w.push_back(343.0 / 45000.0);
+    }
+    for (int i = 0; i < 4; ++i)
+      for (int j = i + 1; j < 4; ++j) {
+        std::vector<double> bb(4, lo);
+        bb[i] = hi;
+        bb[j] = hi;
+        bary.push_back(bb);
+        w.push_back(56.0 / 2250.0);
+      }
+  }
+  const int nq = (int)w.size();
+  const int E2[3][2] = {{0, 1}, {1, 2}, {2, 0}};
+  const int E3[6][2] = {{0, 1}, {1, 2}, {0, 2}, {0, 3}, {1, 3}, {2, 3}};
+  std::vector<double> phi(nq * nl);
+  for (int q = 0; q < nq; ++q) {
+    double sum = 0;
+    for (int c = 1; c <= dim; ++c) sum += bary[q][c];
+    double L[4];
+    L[0] = 1.0 - sum;
+    for (int c = 1; c <= dim; ++c) L[c] = bary[q][c];
+    for (int v = 0; v <= dim; ++v) phi[q * nl + v] = L[v] * (2.0 * L[v] - 1.0);
+    for (int e = 0; e < nl - dim - 1; ++e) {
+      const int i = dim == 2 ? E2[e][0] : E3[e][0], j = dim == 2 ? E2[e][1] : E3[e][1];
+      phi[q * nl + dim + 1 + e] = 4.0 * L[i] * L[j];
+    }
+  }
+  SS_CUDA(cudaMemcpyToSymbolAsync(c_qw, w.data(), sizeof(double) * nq, 0, cudaMemcpyHostToDevice, st));
+  SS_CUDA(cudaMemcpyToSymbolAsync(c_phi, phi.data(), sizeof(double) * nq * nl, 0, cudaMemcpyHostToDevice, st));
+  const int nblk = (int)((P->ne + 255) / 256);
+  double* part = nullptr;
+  SS_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * nblk * nb, st));
+  dim3 grid(nblk, nb);
+  if (dim == 2)
+    k_l2_partials<2><<<grid, 256, 0, st>>>(P->d_conn, P->d_vnodes, P->ne, P->nvn, ncomp, nq, (const double2*)fields_dev, part);
+  else
+    k_l2_partials<3><<<grid, 256, 0, st>>>(P->d_conn, P->d_vnodes, P->ne, P->nvn, ncomp, nq, (const double2*)fields_dev, part);
+  SS_LAUNCH_CHECK();
+  std::vector<double> h((size_t)nblk * nb);
+  SS_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+  SS_CUDA(cudaFreeAsync(part, st));
+  SS_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < nb; ++b) {
+    double acc = 0;
+    for (int q = 0; q < nblk; ++q) acc += h[(size_t)b * nblk + q];
+    out_host[b] = std::sqrt(acc);
+  }
+  return SS_OK;
+}
