@@ -56,6 +56,11 @@ int ss_pattern_export(const ss_pattern* p, int32_t* indptr_host, int32_t* indice
  * counts[i] receives the nnz of rows[i]; indices (capacity cap, may be NULL) the concatenated columns. */
 int ss_pattern_export_rows(const ss_pattern* p, int64_t nrows, const int64_t* rows_host, int64_t* counts_host,
                            int32_t* indices_host, int64_t cap);
+/* Constrained rows a_full[fixed_idx] at frequency omega in the unreduced numbering
+ * (ComplexSaddleSystem.constrained_rows, assembly.py:471-476,491): info_out = {nrows, nnz};
+ * pass NULL arrays to query sizes.  data: nnz complex. */
+int ss_constrained_rows(const ss_pattern* p, double omega, int64_t* info_out, int64_t* indptr_host,
+                        int32_t* indices_host, double* data_host);
 /* ComplexSaddleSystem.vel_dof (n_vel_nodes x dim) and .pres_dof (n_vertices) (assembly.py:319-320). */
 int ss_pattern_dof_maps(const ss_pattern* p, int64_t* vel_dof_host, int64_t* pres_dof_host);
 

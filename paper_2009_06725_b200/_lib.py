@@ -38,6 +38,7 @@ SIGNATURES = {
     "ss_pattern_info": (I32, [P, PI64]),
     "ss_pattern_export": (I32, [P, PI32, PI32]),
     "ss_pattern_dof_maps": (I32, [P, PI64, PI64]),
+    "ss_constrained_rows": (I32, [P, D, PI64, PI64, PI32, PD]),
     "ss_pattern_export_rows": (I32, [P, I64, PI64, PI64, PI32, I64]),
     "ss_assemble": (I32, [P, PD, D, D, P]),
     "ss_export_values": (I32, [P, D, P, P]),

@@ -234,6 +234,21 @@ class SaddleOperator:
                   _lib.ptr(idx, C.c_int32), idx.size)
         return np.split(idx[: int(counts.sum())], np.cumsum(counts)[:-1])
 
+    def constrained_rows(self, omega: float):
+        """scipy CSR of a_full[fixed_idx] at ``omega`` (assembly.py:471-476,491)."""
+        import scipy.sparse as sp
+
+        info = np.zeros(2, dtype=np.int64)
+        _lib.call("ss_constrained_rows", self._h, float(omega), _lib.ptr(info, C.c_int64), None, None, None)
+        nrows, nnz = int(info[0]), int(info[1])
+        ip = np.zeros(nrows + 1, dtype=np.int64)
+        ix = np.zeros(max(1, nnz), dtype=np.int32)
+        data = np.zeros(max(1, nnz), dtype=complex)
+        _lib.call("ss_constrained_rows", self._h, float(omega), _lib.ptr(info, C.c_int64), _lib.ptr(ip, C.c_int64),
+                  _lib.ptr(ix, C.c_int32), _lib.ptr(data.view(np.float64)))
+        ncols = self.n_vel_nodes * self.dim + self.n_vertices
+        return sp.csr_matrix((data[:nnz], ix[:nnz], ip), shape=(nrows, ncols))
+
     def dof_maps(self):
         if self._dof is None:
             vd = np.zeros((self.n_vel_nodes, self.dim), dtype=np.int64)
@@ -390,6 +405,7 @@ class ModeSystemBatch:
     rhs: object              # (nb, ld) complex128 device tensor
     g: object                # (nb, n_vn, dim) complex128 device tensor or None
     dirichlet: list          # per-mode host nodal Dirichlet arrays (None = zero)
+    loads: list = None       # per-mode host traction loads (None = zero)
 
     @property
     def nb(self):
@@ -423,21 +439,23 @@ def assemble_mode_systems(qmesh, props: FluidProps, omegas, g_modes=None, h_mode
     for g in gl:
         _check_dirichlet(op, g)
     loads = None
+    load_host = [None] * nb
     if any(h for h in hl):
         host = np.stack([_traction_loads(qmesh, h) for h in hl])
+        load_host = list(host)
         loads = torch.from_numpy(host).to(op.device)
     gdev = None
     if any(g is not None for g in gl):
         host = np.stack([np.zeros((qmesh.n_velocity_nodes, qmesh.dim), complex) if g is None else g for g in gl])
         gdev = torch.from_numpy(host).to(op.device)
     rhs = op.rhs(omegas, loads, gdev)
-    return ModeSystemBatch(op, omegas, rhs, gdev, gl)
+    return ModeSystemBatch(op, omegas, rhs, gdev, gl, load_host)
 
 
 class ComplexSaddleSystem:
     """Reduced complex saddle-point system of one mode (assembly.py:312-379), device-backed."""
 
-    def __init__(self, operator: SaddleOperator, omega: float, rhs_dev, g_dev, g_host):
+    def __init__(self, operator: SaddleOperator, omega: float, rhs_dev, g_dev, g_host, load_host=None):
         self.operator = operator
         self.omega = float(omega)
         self._rhs_dev = rhs_dev            # (1, ld)
@@ -449,8 +467,10 @@ class ComplexSaddleSystem:
         self.dirichlet_values = store
         self.vel_dof, self.pres_dof = operator.dof_maps()
         self.pinned_pressure = operator.pinned
+        self._load = load_host
         self._rhs = None
         self._matrix = None
+        self._constrained = None
 
     @property
     def rhs(self) -> np.ndarray:
@@ -506,10 +526,27 @@ class ComplexSaddleSystem:
 
     @property
     def constrained_rows(self):
-        raise NotImplementedError("constrained rows (reaction forces) are outside the B200 hot path")
+        """a_full[fixed_idx] as scipy CSR (assembly.py:322,491), device-assembled."""
+        if self._constrained is None:
+            self._constrained = self.operator.constrained_rows(self.omega)
+        return self._constrained
 
-    def reaction_forces(self, x):
-        raise NotImplementedError("reaction forces are outside the B200 hot path (SURVEY.md §2)")
+    @property
+    def constrained_rhs(self) -> np.ndarray:
+        """rhs_full[fixed_idx] (assembly.py:323,492): traction load at fixed DOFs, 0 for a pinned pressure."""
+        op = self.operator
+        fixed_idx = (op.fixed_nodes[:, None] * op.dim + np.arange(op.dim)).ravel()
+        load = np.zeros(op.n_vel_nodes * op.dim, dtype=complex) if self._load is None else self._load.ravel()
+        out = load[fixed_idx]
+        if op.pinned:
+            out = np.concatenate([out, [0.0]])
+        return np.asarray(out, dtype=complex)
+
+    def reaction_forces(self, x: np.ndarray) -> np.ndarray:
+        """Nodal forces on constrained velocity DOFs (assembly.py:364-367)."""
+        u, p = self.expand(x)
+        full = np.concatenate([u.ravel(), p])
+        return np.asarray(self.constrained_rows @ full - self.constrained_rhs)
 
     def export_matrix(self, path) -> None:
         """Coordinate-list text dump ``row col re im`` (assembly.py:373-379)."""
@@ -531,4 +568,5 @@ def assemble_mode_system(qmesh, props: FluidProps, omega: float, g_mode=None, h_
         raise NotImplementedError("the symmetric viscous form is outside the B200 hot path (SURVEY.md §8a row 5)")
     batch = assemble_mode_systems(qmesh, props, [omega], None if g_mode is None else [g_mode],
                                   None if h_mode is None else [h_mode])
-    return ComplexSaddleSystem(batch.operator, omega, batch.rhs, batch.g, batch.dirichlet[0])
+    return ComplexSaddleSystem(batch.operator, omega, batch.rhs, batch.g, batch.dirichlet[0],
+                               None if batch.loads is None else batch.loads[0])

@@ -113,7 +113,8 @@ extern "C" int ss_reference_tables(int dim, double* mref, double* sref, double* 
 template <int DIM>
 __global__ void k_assemble_color(SsOperatorDev op, const int* __restrict__ conn, const int* __restrict__ emap,
                                  int emap_stride, const int* __restrict__ elems, int count,
-                                 const double* __restrict__ vnodes, double rho, double mu, int* flag) {
+                                 const double* __restrict__ vnodes, double rho, double mu, int* flag,
+                                 double2* __restrict__ xsm, double* __restrict__ xdp, double* __restrict__ pinv) {
   constexpr int NL = DIM == 2 ? 6 : 10, NV = DIM + 1;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
@@ -175,7 +176,7 @@ __global__ void k_assemble_color(SsOperatorDev op, const int* __restrict__ conn,
 #pragma unroll
         for (int n = 0; n < DIM; ++n) s += c_sref[((a * NL + b) * DIM + m) * DIM + n] * G[m][n];
       const double sv = smu * s, mv = srho * c_mref[a * NL + b];
-      double2* dst = slot >= 0 ? op.sm + slot : op.lsm + (-2 - slot);
+      double2* dst = slot >= SS_FIXED_BASE ? xsm + (slot - SS_FIXED_BASE) : slot >= 0 ? op.sm + slot : op.lsm + (-2 - slot);
       double2 cur = *dst;
       cur.x += sv;
       cur.y += mv;
@@ -194,8 +195,10 @@ __global__ void k_assemble_color(SsOperatorDev op, const int* __restrict__ conn,
 #pragma unroll
         for (int m = 0; m < DIM; ++m) s += c_tref[(a * DIM + m) * NV + p] * inv[m][d];
         const double dv = -(adet * s);
-        if (s_vp >= 0) op.dp[(size_t)s_vp * DIM + d] += dv;
-        if (s_pv >= 0) op.dt[(size_t)s_pv * DIM + d] += dv;
+        if (s_vp >= SS_FIXED_BASE) xdp[(size_t)(s_vp - SS_FIXED_BASE) * DIM + d] += dv;
+        else if (s_vp >= 0) op.dp[(size_t)s_vp * DIM + d] += dv;
+        if (s_pv >= SS_FIXED_BASE) pinv[(size_t)(s_pv - SS_FIXED_BASE) * DIM + d] += dv;
+        else if (s_pv >= 0) op.dt[(size_t)s_pv * DIM + d] += dv;
         else if (s_pv <= -2) op.ldt[(size_t)(-2 - s_pv) * DIM + d] += dv;
       }
     }
@@ -228,16 +231,19 @@ extern "C" int ss_assemble(ss_pattern* P, const double* vertex_nodes, double den
   SS_CUDA(cudaMemsetAsync(op.lsm, 0, sizeof(double2) * std::max<size_t>(1, P->lcol.size()), st));
   SS_CUDA(cudaMemsetAsync(op.ldt, 0, sizeof(double) * std::max<size_t>(1, P->ltcol.size() * P->dim), st));
   SS_CUDA(cudaMemsetAsync(P->d_flag, 0, sizeof(int), st));
+  SS_CUDA(cudaMemsetAsync(P->d_xsm, 0, sizeof(double2) * std::max<size_t>(1, P->xcol.size()), st));
+  SS_CUDA(cudaMemsetAsync(P->d_xdp, 0, sizeof(double) * std::max<size_t>(1, P->xpcol.size() * P->dim), st));
+  SS_CUDA(cudaMemsetAsync(P->d_pinv, 0, sizeof(double) * std::max<size_t>(1, P->pincol.size() * P->dim), st));
   for (int k = 0; k < P->ncolors; ++k) {
     const int off = P->color_ptr[k], cnt = P->color_ptr[k + 1] - off;
     if (cnt == 0) continue;
     const int bs = 128, gs = (cnt + bs - 1) / bs;
     if (P->dim == 2)
       k_assemble_color<2><<<gs, bs, 0, st>>>(op, P->d_conn, P->d_emap, P->emap_stride, P->d_color_elems + off,
-                                             cnt, P->d_vnodes, density, viscosity, P->d_flag);
+                                             cnt, P->d_vnodes, density, viscosity, P->d_flag, P->d_xsm, P->d_xdp, P->d_pinv);
     else
       k_assemble_color<3><<<gs, bs, 0, st>>>(op, P->d_conn, P->d_emap, P->emap_stride, P->d_color_elems + off,
-                                             cnt, P->d_vnodes, density, viscosity, P->d_flag);
+                                             cnt, P->d_vnodes, density, viscosity, P->d_flag, P->d_xsm, P->d_xdp, P->d_pinv);
     SS_LAUNCH_CHECK();
   }
   k_gather_diag<<<(P->nfree + 255) / 256, 256, 0, st>>>(op);

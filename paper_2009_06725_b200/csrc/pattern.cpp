@@ -192,7 +192,37 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
   }
   nodes_rows.clear(); vert_rows.clear(); prow_nodes.clear();
 
+  // Constrained rows a_full[fixed_idx] (assembly.py:471-476,491): rows of fixed velocity nodes
+  // (all node / vertex neighbours, global ids) and, if the pressure is pinned, the row of vertex 0.
+  {
+    std::vector<int> fixed;
+    for (int64_t A = 0; A < n_vel_nodes; ++A) if (P->rank[A] < 0) fixed.push_back((int)A);
+    P->fixed_nodes = fixed;
+    P->frank.assign(n_vel_nodes, -1);
+    for (size_t i = 0; i < fixed.size(); ++i) P->frank[fixed[i]] = (int)i;
+    std::vector<std::vector<int>> xn, xv, pin;
+    collect_rows(fixed, inc_ptr, inc, vel_conn, nloc, nloc, xn);
+    collect_rows(fixed, inc_ptr, inc, vel_conn, nloc, nvloc, xv);
+    P->xptr.assign(fixed.size() + 1, 0);
+    P->xpptr.assign(fixed.size() + 1, 0);
+    for (size_t i = 0; i < fixed.size(); ++i) {
+      P->xptr[i + 1] = P->xptr[i] + (int)xn[i].size();
+      P->xpptr[i + 1] = P->xpptr[i] + (int)xv[i].size();
+    }
+    for (size_t i = 0; i < fixed.size(); ++i) {
+      P->xcol.insert(P->xcol.end(), xn[i].begin(), xn[i].end());
+      P->xpcol.insert(P->xpcol.end(), xv[i].begin(), xv[i].end());
+    }
+    if (P->pinned) {
+      std::vector<int> v0 = {0};
+      collect_rows(v0, inc_ptr, inc, vel_conn, nloc, nloc, pin);
+      P->pincol = pin[0];
+    }
+  }
+
   // Element -> slot maps: [vv nloc*nloc][vp nloc*nvloc][pv nvloc*nloc] per element.
+  // Codes: >= 0 free-row slot, <= -2 Dirichlet-lift slot, >= SS_FIXED_BASE constrained-row slot
+  // (fixed velocity rows for vv/vp, the pinned pressure row for pv), -1 unused.
   const int per = nloc * nloc + 2 * nloc * nvloc;
   P->emap_stride = per;
   P->emap.assign((size_t)n_elements * per, -1);
@@ -211,14 +241,21 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
           } else {
             s = -(2 + P->lptr[rA] + lb(P->lcol.data() + P->lptr[rA], P->lptr[rA + 1] - P->lptr[rA], B));
           }
+        } else {
+          const int f = P->frank[A];
+          s = SS_FIXED_BASE + P->xptr[f] + lb(P->xcol.data() + P->xptr[f], P->xptr[f + 1] - P->xptr[f], B);
         }
         m[a * nloc + b] = s;
       }
       for (int q = 0; q < nvloc; ++q) {
         const int pd = P->vert_pdof[c[q]];
         int s = -1;
-        if (rA >= 0 && pd >= 0)
+        if (rA >= 0 && pd >= 0) {
           s = P->pptr[rA] + lb(P->pcol.data() + P->pptr[rA], P->pptr[rA + 1] - P->pptr[rA], pd);
+        } else if (rA < 0) {
+          const int f = P->frank[A];
+          s = SS_FIXED_BASE + P->xpptr[f] + lb(P->xpcol.data() + P->xpptr[f], P->xpptr[f + 1] - P->xpptr[f], (int)c[q]);
+        }
         m[nloc * nloc + a * nvloc + q] = s;
       }
     }
@@ -232,6 +269,8 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
             s = P->tptr[pd] + lb(P->tcol.data() + P->tptr[pd], P->tptr[pd + 1] - P->tptr[pd], rA);
           else
             s = -(2 + P->ltptr[pd] + lb(P->ltcol.data() + P->ltptr[pd], P->ltptr[pd + 1] - P->ltptr[pd], A));
+        } else if (P->pinned && c[q] == 0) {
+          s = SS_FIXED_BASE + lb(P->pincol.data(), (int)P->pincol.size(), A);
         }
         m[nloc * nloc + nloc * nvloc + q * nloc + a] = s;
       }
@@ -292,6 +331,9 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
   if ((rc = alloc_zero(P, P->lcol.size(), &op.lsm))) { delete P; return rc; }
   if ((rc = alloc_zero(P, P->ltcol.size() * dim, &op.ldt))) { delete P; return rc; }
   if ((rc = alloc_zero(P, (size_t)n_vertices * dim, &P->d_vnodes))) { delete P; return rc; }
+  if ((rc = alloc_zero(P, P->xcol.size(), &P->d_xsm))) { delete P; return rc; }
+  if ((rc = alloc_zero(P, P->xpcol.size() * dim, &P->d_xdp))) { delete P; return rc; }
+  if ((rc = alloc_zero(P, P->pincol.size() * dim, &P->d_pinv))) { delete P; return rc; }
   if ((rc = alloc_zero(P, 4, &P->d_flag))) { delete P; return rc; }
   *out = P;
   return SS_OK;
@@ -480,6 +522,61 @@ extern "C" int ss_pattern_export_rows(const ss_pattern* P, int64_t nrows, const 
       }
     }
     counts[i] = c;
+  }
+  return SS_OK;
+}
+
+
+// Constrained rows a_full[fixed_idx] in the unreduced numbering (assembly.py:471-476,491): one row
+// per (fixed node, component) in ascending order, then the pinned pressure row if any.  Columns are
+// sorted full indices (velocity B*dim+d, pressure n_vel_nodes*dim + P); explicit zeros kept.
+// indptr (nrows+1) / indices / data (complex) may be NULL to query sizes via info_out[2] = {nrows, nnz}.
+extern "C" int ss_constrained_rows(const ss_pattern* P, double omega, int64_t* info_out, int64_t* indptr,
+                                   int32_t* indices, double* data) {
+  if (!P || !info_out) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  const int dim = P->dim;
+  const int64_t nf = (int64_t)P->fixed_nodes.size();
+  const int64_t nrows = nf * dim + (P->pinned ? 1 : 0);
+  const int64_t nnz = (int64_t)dim * ((int64_t)P->xcol.size() + (int64_t)P->xpcol.size()) +
+                      (int64_t)dim * (int64_t)P->pincol.size();
+  info_out[0] = nrows;
+  info_out[1] = nnz;
+  if (!indptr || !indices || !data) return SS_OK;
+  std::vector<double2> xsm(P->xcol.size());
+  std::vector<double> xdp(P->xpcol.size() * dim), pinv(P->pincol.size() * dim);
+  if (!xsm.empty()) SS_CUDA(cudaMemcpy(xsm.data(), P->d_xsm, sizeof(double2) * xsm.size(), cudaMemcpyDeviceToHost));
+  if (!xdp.empty()) SS_CUDA(cudaMemcpy(xdp.data(), P->d_xdp, sizeof(double) * xdp.size(), cudaMemcpyDeviceToHost));
+  if (!pinv.empty()) SS_CUDA(cudaMemcpy(pinv.data(), P->d_pinv, sizeof(double) * pinv.size(), cudaMemcpyDeviceToHost));
+  const int64_t pbase = P->nvn * dim;
+  int64_t pos = 0, row = 0;
+  indptr[0] = 0;
+  for (int64_t i = 0; i < nf; ++i) {
+    for (int d = 0; d < dim; ++d) {
+      for (int e = P->xptr[i]; e < P->xptr[i + 1]; ++e) {
+        indices[pos] = (int32_t)((int64_t)P->xcol[e] * dim + d);
+        data[2 * pos] = xsm[e].x;
+        data[2 * pos + 1] = omega == 0.0 ? 0.0 : omega * xsm[e].y;
+        ++pos;
+      }
+      for (int e = P->xpptr[i]; e < P->xpptr[i + 1]; ++e) {
+        indices[pos] = (int32_t)(pbase + P->xpcol[e]);
+        data[2 * pos] = xdp[(size_t)e * dim + d];
+        data[2 * pos + 1] = 0.0;
+        ++pos;
+      }
+      indptr[++row] = pos;
+    }
+  }
+  if (P->pinned) {
+    for (size_t e = 0; e < P->pincol.size(); ++e)
+      for (int d = 0; d < dim; ++d) {
+        indices[pos] = (int32_t)((int64_t)P->pincol[e] * dim + d);
+        data[2 * pos] = pinv[e * dim + d];
+        data[2 * pos + 1] = 0.0;
+        ++pos;
+      }
+    indptr[++row] = pos;
   }
   return SS_OK;
 }

@@ -4,6 +4,8 @@
 
 #include "ss_common.h"
 
+constexpr int SS_FIXED_BASE = 1 << 30;   // element-map code offset of constrained-row slots
+
 struct ss_pattern {
   int device = 0;
   int dim = 0, nloc = 0, nvloc = 0;
@@ -14,6 +16,11 @@ struct ss_pattern {
   std::vector<int> rank, free_nodes, vert_pdof, pres_of_row;
   std::vector<int> nptr, ncol, pptr, pcol, tptr, tcol, lptr, lcol, ltptr, ltcol, diag_slot;
   std::vector<int> emap, color_ptr, color_elems;
+  // constrained rows (fixed velocity nodes; pinned pressure row)
+  std::vector<int> fixed_nodes, frank, xptr, xcol, xpptr, xpcol, pincol;
+  double2* d_xsm = nullptr;
+  double* d_xdp = nullptr;
+  double* d_pinv = nullptr;
   // device
   SsOperatorDev op{};
   int* d_conn = nullptr;         // int32 vel_conn

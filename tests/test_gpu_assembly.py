@@ -179,3 +179,45 @@ def test_omega_zero_real_and_symmetric(small_channel_qmesh, fluid):
     n_u = s2.n_velocity_dofs
     blk = s2.matrix.tocsc()[n_u:, n_u:]
     assert blk.nnz == 0 or np.abs(blk.data).max() == 0.0
+
+
+def _rows_close(a, b, tol=1e-13):
+    a, b = a.tocsr(), b.tocsr()
+    assert a.shape == b.shape
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+    assert np.abs(a.data - b.data).max() <= tol * np.abs(b.data).max()
+
+
+def test_constrained_rows_and_reaction_forces(fluid):
+    """a_full[fixed_idx], rhs_full[fixed_idx] and the momentum balance (assembly.py:364-367,491-492)."""
+    from paper_2009_06725_b200.krylov import SolverSettings, gmres_solve
+    from paper_2009_06725_b200.mesh import promote_to_quadratic
+    from paper_2009_06725_b200.structured import channel_grid
+
+    q = promote_to_quadratic(channel_grid(8, 4, length=4.0, half_height=1.0))
+    h = {"inlet": np.array([1.0, 0.0])}
+    system = assemble_mode_system(q, fluid, 0.0, h_mode=h)
+    ref = oracle.assemble_mode_system(q, fluid.density, fluid.viscosity, 0.0, h_mode=h)
+    _rows_close(system.constrained_rows, ref.constrained_rows)
+    np.testing.assert_allclose(system.constrained_rhs, ref.constrained_rhs, rtol=1e-14, atol=1e-15)
+    x, _ = gmres_solve(system, SolverSettings(tolerance=1e-12))
+    total = system.reaction_forces(x).reshape(-1, 2).sum(axis=0)
+    assert total[0].real == pytest.approx(-2.0, rel=1e-9)      # reference test_assembly.py:226-236
+    assert abs(total[1]) < 1e-9
+    s2 = assemble_mode_system(q, fluid, 3.0, h_mode=h)
+    _rows_close(s2.constrained_rows, oracle.assemble_mode_system(q, 1.0, 1.0, 3.0, h_mode=h).constrained_rows)
+
+
+def test_constrained_rows_with_pinned_pressure_3d():
+    case = pipe3d_case()
+    props = FluidProps(case.density, case.viscosity)
+    from paper_2009_06725_b200.mesh import with_patch_kinds, promote_to_quadratic
+
+    m = with_patch_kinds(case.mesh, {"outlet": "dirichlet"})          # no Neumann patch -> pinned
+    q = promote_to_quadratic(m, case.geometry)
+    g = case.coefficients[2] * case.profile
+    s = assemble_mode_system(q, props, case.omegas[2], g_mode=g)
+    assert s.pinned_pressure
+    ref = oracle.assemble_mode_system(q, case.density, case.viscosity, case.omegas[2], g_mode=g)
+    _rows_close(s.constrained_rows, ref.constrained_rows)
+    assert np.array_equal(s.matrix.indices, ref.matrix.indices)
