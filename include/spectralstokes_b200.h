@@ -87,6 +87,10 @@ int ss_rhs_batched(const ss_pattern* p, int nb, const double* omegas_dev, const 
  * Replaces `matrix @ q` / `scale * (matrix @ q)` (krylov.py:94,108,155; assembly.py:362). */
 int ss_spmv_batched(const ss_pattern* p, int nb, const double* omegas_dev, const double* x_dev,
                     double* y_dev, int64_t ld, int jacobi, void* stream);
+/* Same product with the mode-interleaved input layout the GMRES tick uses: x_dev is [row][nb]
+ * (x[row*nb + b]), y_dev is [b][ld].  Gathers of one node return all modes' values contiguously. */
+int ss_spmv_batched_interleaved(const ss_pattern* p, int nb, const double* omegas_dev, const double* x_dev,
+                                double* y_dev, int64_t ld, int jacobi, void* stream);
 /* Algorithmic bytes of one ss_spmv_batched call over nb modes (roofline numerator). */
 int64_t ss_spmv_bytes(const ss_pattern* p, int nb);
 /* True relative residuals ||b - A x||/||b|| (||A x|| if b = 0) per mode (ComplexSaddleSystem.residual_norm,

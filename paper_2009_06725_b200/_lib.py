@@ -45,6 +45,7 @@ SIGNATURES = {
     "ss_surface_load": (I32, [I32, I64, PD, I64, PI64, I32, PD, PD]),
     "ss_rhs_batched": (I32, [P, I32, P, P, P, P, I64, P]),
     "ss_spmv_batched": (I32, [P, I32, P, P, P, I64, I32, P]),
+    "ss_spmv_batched_interleaved": (I32, [P, I32, P, P, P, I64, I32, P]),
     "ss_spmv_bytes": (I64, [P, I32]),
     "ss_jacobi": (I32, [P, I32, P, P, I64, P]),
     "ss_residual_norms": (I32, [P, I32, P, P, P, I64, PD, P]),

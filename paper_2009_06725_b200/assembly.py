@@ -308,6 +308,18 @@ class SaddleOperator:
                   _lib.ptr(out), _lib.stream_ptr(self.device))
         return out
 
+    def spmv_interleaved(self, omegas, x_int, jacobi=False, out=None):
+        """Mode-interleaved SpMV (the GMRES tick's kernel): x_int (ld, nb) row-major, returns (nb, ld)."""
+        torch = _lib.torch_mod()
+        om = self._omegas(omegas)
+        nb = om.numel()
+        if tuple(x_int.shape) != (self.ld, nb) or x_int.dtype != torch.complex128:
+            raise ValueError(f"x_int must be ({self.ld}, {nb}) complex128")
+        y = torch.zeros((nb, self.ld), dtype=torch.complex128, device=self.device) if out is None else out
+        _lib.call("ss_spmv_batched_interleaved", self._h, nb, _lib.dptr(om), _lib.dptr(x_int.contiguous()),
+                  _lib.dptr(y), self.ld, int(bool(jacobi)), _lib.stream_ptr(self.device))
+        return y
+
     def spmv_bytes(self, nb: int) -> int:
         return int(_lib.load().ss_spmv_bytes(self._h, nb))
 

@@ -447,6 +447,32 @@ extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas
   return SS_OK;
 }
 
+// Standalone mode-interleaved batched SpMV (the GMRES tick's SpMV): X[row][nb] -> Y[b][ld].
+template <int DIM>
+__global__ void __launch_bounds__(256) k_spmv_interleaved(SsOperatorDev op, int nb, const double* __restrict__ omegas,
+                                                          const double2* __restrict__ X, double2* __restrict__ Y,
+                                                          int64_t ld, int jacobi, int split) {
+  const int blk = blockIdx.x / split, sub = blockIdx.x % split;
+  saddle_block_interleaved<DIM>(op, blk, sub, split, nb, nb, X, Y, ld, jacobi, [](int) { return true; },
+                                [&](int m) { return omegas[m]; }, [](int) { return 1.0; });
+}
+
+extern "C" int ss_spmv_batched_interleaved(const ss_pattern* P, int nb, const double* omegas_dev, const double* x_dev,
+                                           double* y_dev, int64_t ld, int jacobi, void* stream_) {
+  if (!P || !x_dev || !y_dev || !omegas_dev || nb <= 0 || ld < P->op.n) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int nsb = saddle_nsb_host(P->nfree, P->npf);
+  const int split = std::max(1, std::min(16, (8 * 148 + nsb - 1) / nsb));
+  const unsigned grid = (unsigned)(nsb * split);
+  if (P->dim == 2)
+    k_spmv_interleaved<2><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi, split);
+  else
+    k_spmv_interleaved<3><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi, split);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
 // Algorithmic bytes of one standalone SpMV over nb modes.
 extern "C" int64_t ss_spmv_bytes(const ss_pattern* P, int nb) {
   const int64_t dim = P->dim;

@@ -189,100 +189,13 @@ __global__ void __launch_bounds__(PT) k_init(KArgs a) {
 // ------------------------------------------------------------------------------------------------
 constexpr int MAXB_SMEM = 256;   // modes whose per-tick state is cached in shared memory
 
-__device__ __forceinline__ double2 ldnc2(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-
-// Threads walk the (row, mode) pairs of the block, mode fastest: a warp covers one or two rows for
-// every mode of the batch, so matrix loads are broadcasts and the P gathers are contiguous runs.
 template <int DIM>
 __device__ __forceinline__ void spmv_inner_interleaved(const KArgs& a, int blk, const int* sph,
                                                        const double* som, const double* sxs) {
-  const SsOperatorDev& op = a.op;
-  const int nb = a.nb, ps = a.pstride;
-  const int sub = blockIdx.x % a.spmv_split;
-  const int nvb = saddle_nvb(op);
-  const bool vel = blk < nvb;
-  const int r0 = vel ? blk * SPMV_VROWS : (blk - nvb) * SPMV_PROWS;
-  const int rend = vel ? min(r0 + SPMV_VROWS, op.nfree) : min(r0 + SPMV_PROWS, op.npf);
-  const int npairs = (rend - r0) * nb;
-  for (int pr = sub * PT + threadIdx.x; pr < npairs; pr += a.spmv_split * PT) {
-    const int r = r0 + pr / nb, m = pr % nb;
-    const int ph = sph[m];
-    if (ph != PH_INNER && ph != PH_START) continue;
-    const double om = som[m], xs = sxs[m];
-    const double2* P = a.P + m;
-    double2* w = a.W + (size_t)m * a.ld;
-    if (vel) {
-      double2 acc[DIM];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
-      const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-      int e = e0;
-      for (; e + 4 <= e1; e += 4) {
-        int B[4];
-        double2 sm[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { B[u] = __ldg(op.ncol + e + u); sm[u] = __ldg(op.sm + e + u); }
-        double2 v[4][DIM];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) v[u][d] = ldnc2(P + ((size_t)B[u] * DIM + d) * ps);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double am = om * sm[u].y;
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            acc[d].x += sm[u].x * v[u][d].x - am * v[u][d].y;
-            acc[d].y += sm[u].x * v[u][d].y + am * v[u][d].x;
-          }
-        }
-      }
-      for (; e < e1; ++e) {
-        const int B = __ldg(op.ncol + e);
-        const double2 sm = __ldg(op.sm + e);
-        const double am = om * sm.y;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          const double2 v = ldnc2(P + ((size_t)B * DIM + d) * ps);
-          acc[d].x += sm.x * v.x - am * v.y;
-          acc[d].y += sm.x * v.y + am * v.x;
-        }
-      }
-      const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
-#pragma unroll 4
-      for (int q = p0; q < p1; ++q) {
-        const double2 v = ldnc2(P + (size_t)(op.nfv + __ldg(op.pcol + q)) * ps);
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          const double dv = __ldg(op.dp + (size_t)q * DIM + d);
-          acc[d].x += dv * v.x;
-          acc[d].y += dv * v.y;
-        }
-      }
-      const double2 sj = a.jacobi ? saddle_jacobi(op, r, om) : make_double2(1.0, 0.0);
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) w[(size_t)r * DIM + d] = cmul(sj, cscale(acc[d], xs));
-    } else {
-      double2 acc = make_double2(0.0, 0.0);
-      const int e0 = __ldg(op.tptr + r), e1 = __ldg(op.tptr + r + 1);
-#pragma unroll 4
-      for (int e = e0; e < e1; ++e) {
-        const double2* xb = P + (size_t)__ldg(op.tcol + e) * DIM * ps;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          const double dv = __ldg(op.dt + (size_t)e * DIM + d);
-          const double2 v = ldnc2(xb + (size_t)d * ps);
-          acc.x += dv * v.x;
-          acc.y += dv * v.y;
-        }
-      }
-      w[op.nfv + r] = cscale(acc, xs);
-    }
-  }
+  saddle_block_interleaved<DIM>(
+      a.op, blk, blockIdx.x % a.spmv_split, a.spmv_split, a.nb, a.pstride, a.P, a.W, a.ld, a.jacobi,
+      [&](int m) { return sph[m] == PH_INNER || sph[m] == PH_START; },
+      [&](int m) { return som[m]; }, [&](int m) { return sxs[m]; });
 }
 
 // RESID for one mode (row layout X): t = b - A x, r = s.t -> P (interleaved) and Q[0]; norms.

@@ -224,3 +224,100 @@ __device__ __forceinline__ void csr_block(const SsCsrDev& A, int set, int blk, c
     }
   }
 }
+
+__device__ __forceinline__ double2 ldnc2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// Mode-interleaved batched SpMV over one row block (the GMRES tick's inner SpMV and the
+// standalone ss_spmv_batched_interleaved).  x is [row][ps] (column m = mode m), y is [m][ld].
+// Threads walk the block's (row, mode) pairs, mode fastest: matrix loads are broadcasts and the
+// x gathers contiguous runs over the batch.  Each (row, mode) is summed by one thread in entry
+// order (deterministic, independent of the batch).  active(m) selects modes; scale(m) multiplies.
+template <int DIM, class Active, class Omega, class Scale>
+__device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op, int blk, int sub, int split,
+                                                         int nb, int ps, const double2* __restrict__ x,
+                                                         double2* __restrict__ y, int64_t ld, int jacobi,
+                                                         Active active, Omega omega_of, Scale scale_of) {
+  const int nvb = saddle_nvb(op);
+  const bool vel = blk < nvb;
+  const int r0 = vel ? blk * SPMV_VROWS : (blk - nvb) * SPMV_PROWS;
+  const int rend = vel ? min(r0 + SPMV_VROWS, op.nfree) : min(r0 + SPMV_PROWS, op.npf);
+  const int npairs = (rend - r0) * nb;
+  for (int pr = sub * blockDim.x + threadIdx.x; pr < npairs; pr += split * blockDim.x) {
+    const int r = r0 + pr / nb, m = pr % nb;
+    if (!active(m)) continue;
+    const double om = omega_of(m), xs = scale_of(m);
+    const double2* P = x + m;
+    double2* w = y + (size_t)m * ld;
+    if (vel) {
+      double2 acc[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
+      const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
+      int e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        int B[4];
+        double2 sm[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { B[u] = __ldg(op.ncol + e + u); sm[u] = __ldg(op.sm + e + u); }
+        double2 v[4][DIM];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) v[u][d] = ldnc2(P + ((size_t)B[u] * DIM + d) * ps);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double am = om * sm[u].y;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            acc[d].x += sm[u].x * v[u][d].x - am * v[u][d].y;
+            acc[d].y += sm[u].x * v[u][d].y + am * v[u][d].x;
+          }
+        }
+      }
+      for (; e < e1; ++e) {
+        const int B = __ldg(op.ncol + e);
+        const double2 sm = __ldg(op.sm + e);
+        const double am = om * sm.y;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          const double2 v = ldnc2(P + ((size_t)B * DIM + d) * ps);
+          acc[d].x += sm.x * v.x - am * v.y;
+          acc[d].y += sm.x * v.y + am * v.x;
+        }
+      }
+      const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
+#pragma unroll 4
+      for (int q = p0; q < p1; ++q) {
+        const double2 v = ldnc2(P + (size_t)(op.nfv + __ldg(op.pcol + q)) * ps);
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          const double dv = __ldg(op.dp + (size_t)q * DIM + d);
+          acc[d].x += dv * v.x;
+          acc[d].y += dv * v.y;
+        }
+      }
+      const double2 sj = jacobi ? saddle_jacobi(op, r, om) : make_double2(1.0, 0.0);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) w[(size_t)r * DIM + d] = cmul(sj, cscale(acc[d], xs));
+    } else {
+      double2 acc = make_double2(0.0, 0.0);
+      const int e0 = __ldg(op.tptr + r), e1 = __ldg(op.tptr + r + 1);
+#pragma unroll 4
+      for (int e = e0; e < e1; ++e) {
+        const double2* xb = P + (size_t)__ldg(op.tcol + e) * DIM * ps;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          const double dv = __ldg(op.dt + (size_t)e * DIM + d);
+          const double2 v = ldnc2(xb + (size_t)d * ps);
+          acc.x += dv * v.x;
+          acc.y += dv * v.y;
+        }
+      }
+      w[op.nfv + r] = cscale(acc, xs);
+    }
+  }
+}

@@ -221,3 +221,21 @@ def test_constrained_rows_with_pinned_pressure_3d():
     ref = oracle.assemble_mode_system(q, case.density, case.viscosity, case.omegas[2], g_mode=g)
     _rows_close(s.constrained_rows, ref.constrained_rows)
     assert np.array_equal(s.matrix.indices, ref.matrix.indices)
+
+
+def test_interleaved_spmv_matches_row_layout_and_oracle(c1):
+    case, props, g = c1
+    op = get_operator(case.qmesh, props)
+    nb = case.n_modes + 1
+    rng = np.random.default_rng(8)
+    x = np.zeros((nb, op.ld), complex)
+    x[:, : op.n] = rng.normal(size=(nb, op.n)) + 1j * rng.normal(size=(nb, op.n))
+    xr = torch.from_numpy(x).cuda()
+    y_row = op.spmv(case.omegas, xr, jacobi=True).cpu().numpy()
+    y_int = op.spmv_interleaved(case.omegas, xr.t().contiguous(), jacobi=True).cpu().numpy()
+    h = case.h_modes()
+    for b in range(nb):
+        s = oracle.assemble_mode_system(case.qmesh, case.density, case.viscosity, case.omegas[b], h_mode=h[b])
+        ref = oracle.jacobi_scale(s.matrix) * (s.matrix @ x[b, : op.n])
+        assert np.linalg.norm(y_int[b, : op.n] - ref) <= 1e-13 * np.linalg.norm(ref)
+        assert np.linalg.norm(y_int[b, : op.n] - y_row[b, : op.n]) <= 1e-14 * np.linalg.norm(ref)
