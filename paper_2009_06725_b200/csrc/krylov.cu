@@ -73,6 +73,7 @@ struct KArgs {
   int* n_done;
   double* hist;                // [b][hist_cap]
   unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
+  long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -422,7 +423,8 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   const int belem = J * RB;
   // passes with an update phase amortise their extra barriers over bigger chunks (measured)
   const int div = a.stage_div > 0 ? a.stage_div : (PASS == PASS_A ? 3 : 2);
-  const int CB = max(1, min(min(nblocks, 8), (a.smem_elems / div) / (belem + RB)));
+  // pass B keeps each thread's basis values in registers between its two phases: one block/chunk
+  const int CB = PASS == PASS_B ? 1 : max(1, min(min(nblocks, 8), (a.smem_elems / div) / (belem + RB)));
   const int stage_elems = CB * (belem + RB);
   const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
   const int nchunks = (nblocks + CB - 1) / CB;
@@ -453,7 +455,41 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
     const int c0 = blk_begin + ci * CB;
     const int nc = min(CB, blk_end - c0);
     double2* Vb = st + CB * belem;
-    if (PASS != PASS_A) {
+    if (PASS == PASS_B) {
+      // phase 1 with the phase-2 distribution (j = warp + 8t, lane = row): Q read from smem once
+      double2 qv[T];
+      const double2* S = st + lane;
+      double2 p = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int j = warp + 8 * t;
+        if (j < J) {
+          qv[t] = S[j * RB];
+          const double2 cf = coef[j];
+          p.x += qv[t].x * cf.x - qv[t].y * cf.y;
+          p.y += qv[t].x * cf.y + qv[t].y * cf.x;
+        } else {
+          qv[t] = make_double2(0.0, 0.0);
+        }
+      }
+      red[tid] = p;
+      __syncthreads();
+      if (warp == 0) {
+        double2 tot = red[lane];
+#pragma unroll
+        for (int w = 1; w < PT / 32; ++w) tot = cadd(tot, red[w * 32 + lane]);
+        const double2 v = csub(Vb[lane], tot);
+        Vb[lane] = v;
+        vec[(int64_t)c0 * RB + lane] = v;
+      }
+      __syncthreads();
+      const double2 v = Vb[lane];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        acc[t].x += qv[t].x * v.x + qv[t].y * v.y;
+        acc[t].y += qv[t].x * v.y - qv[t].y * v.x;
+      }
+    } else if (PASS != PASS_A) {
       for (int cr = 0; cr < nc; cr += 8) {
         const int nr = min(8, nc - cr);
         const int SL = pass_slices(nr);
@@ -488,7 +524,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
         __syncthreads();
       }
     }
-    if (PASS == PASS_A || PASS == PASS_B) {
+    if (PASS == PASS_A) {
       for (int c = 0; c < nc; ++c) {
         const double2* S = st + c * belem + lane;
         const double2 v = Vb[c * RB + lane];
@@ -559,6 +595,7 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     else if (T <= 4) stream_segment<PASS, 4>(a, b, s, J, k, coef, smem, mbar, red, part);
     else if (T <= 8) stream_segment<PASS, 8>(a, b, s, J, k, coef, smem, mbar, red, part);
     else if (T <= 16) stream_segment<PASS, 16>(a, b, s, J, k, coef, smem, mbar, red, part);
+    else if (T <= 26) stream_segment<PASS, 26>(a, b, s, J, k, coef, smem, mbar, red, part);
     else stream_segment<PASS, 32>(a, b, s, J, k, coef, smem, mbar, red, part);
   } else {
     stream_segment<PASS, 1>(a, b, s, J, k, coef, smem, mbar, red, part);
@@ -769,6 +806,7 @@ struct ss_krylov {
   int* h_done = nullptr;       // pinned
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int ticks_per_graph = 8;
+  int device_loop = 0;         // whole solve as one graph with a conditional WHILE node (SS_DEVICE_LOOP=0: host-polled)
   size_t smem_pass = 0;
   int64_t last_ticks = 0;
   int64_t last_launches = 0;
@@ -801,6 +839,7 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   a.smem_elems = PASS_SMEM_ELEMS;
   a.stage_div = 0;   // 0 = per-pass default
   if (const char* e = getenv("SS_PASS_SMEM")) a.smem_elems = std::max(2048, std::min(PASS_SMEM_ELEMS, atoi(e)));
+  a.smem_elems = std::max(a.smem_elems, a.jcap * RB + 2 * RB);   // one full-J block + vector must fit a stage
   if (const char* e = getenv("SS_PASS_DIV")) a.stage_div = std::max(1, atoi(e));
   K->max_batch = max_batch;
   const size_t B = max_batch;
@@ -826,6 +865,7 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if ((rc = kalloc(K, B, &a.ctl))) return rc;
   if ((rc = kalloc(K, B * a.hist_cap, &a.hist))) return rc;
   if ((rc = kalloc(K, 8, &a.bytes))) return rc;
+  if ((rc = kalloc(K, 2, &a.loop))) return rc;
   SS_CUDA(cudaHostAlloc((void**)&K->h_done, 2 * sizeof(int), cudaHostAllocDefault));
   SS_CUDA(cudaStreamCreateWithFlags(&K->cap_stream, cudaStreamNonBlocking));
   SS_CUDA(cudaEventCreateWithFlags(&K->ev[0], cudaEventDisableTiming));
@@ -835,12 +875,16 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     ss_set_error("restart too large for the shared-memory staging of the basis passes");
     return SS_ERR_ARG;
   }
-  auto setattr = [&](const void* f) { return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K->smem_pass); };
+  auto setattr = [&](const void* f) {   // per-function attribute: the largest any workspace may request
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(PASS_SMEM_ELEMS * sizeof(double2)));
+  };
   SS_CUDA(setattr((const void*)k_pass<PASS_A>));
   SS_CUDA(setattr((const void*)k_pass<PASS_B>));
   SS_CUDA(setattr((const void*)k_pass<PASS_C>));
   SS_CUDA(setattr((const void*)k_pass<PASS_X>));
   K->ticks_per_graph = n < 200000 ? 16 : 2;
+  if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
+  if (const char* e = getenv("SS_TICKS_PER_GRAPH")) K->ticks_per_graph = std::max(1, atoi(e));
   return SS_OK;
 }
 
@@ -950,6 +994,55 @@ static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
 
 static int tick_dim(const ss_krylov* K) { return K->a.kind == 0 ? K->a.op.dim : 2; }
 
+// Device-side loop control: after every body of ticks, keep looping while some mode is not done
+// and the tick cap is not reached (the whole solve is ONE graph launch, no host round trips).
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ n_done, int nb,
+                            long long* loop, int per_body) {
+  const long long t = (loop[0] += per_body);
+  cudaGraphSetConditional(h, (*n_done < nb && t < loop[1]) ? 1u : 0u);
+}
+
+static int get_while_graph(ss_krylov* K, int nb, int jacobi, cudaGraphExec_t* out) {
+  const int64_t key = (int64_t)nb * 4 + jacobi * 2 + 1;
+  auto it = K->graphs.find(key);
+  if (it != K->graphs.end()) { *out = it->second; return SS_OK; }
+  KArgs a = K->a;
+  a.nb = nb;
+  a.jacobi = jacobi;
+  cudaGraph_t g;
+  SS_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  SS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  SS_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  SS_CUDA(cudaStreamBeginCaptureToGraph(K->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int rc = SS_OK;
+  for (int t = 0; t < K->ticks_per_graph && !rc; ++t)
+    rc = tick_dim(K) == 3 ? launch_tick<3>(K, a, K->cap_stream) : launch_tick<2>(K, a, K->cap_stream);
+  if (!rc) {
+    k_loop_cond<<<1, 1, 0, K->cap_stream>>>(h, a.n_done, nb, a.loop, K->ticks_per_graph);
+    if (cudaGetLastError() != cudaSuccess) rc = SS_ERR_CUDA;
+  }
+  cudaError_t e = cudaStreamEndCapture(K->cap_stream, &body);
+  if (rc || e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    ss_set_error(std::string("conditional graph capture failed: ") + cudaGetErrorString(e));
+    return rc ? rc : SS_ERR_CUDA;
+  }
+  cudaGraphExec_t ex;
+  SS_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  K->graphs[key] = ex;
+  *out = ex;
+  return SS_OK;
+}
+
 static int get_graph(ss_krylov* K, int nb, int jacobi, cudaGraphExec_t* out) {
   const int64_t key = (int64_t)nb * 4 + jacobi * 2;
   auto it = K->graphs.find(key);
@@ -1014,15 +1107,35 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
   if (tick_dim(K) == 3) k_init<3><<<nb * a.nseg, PT, 0, st>>>(a);
   else k_init<2><<<nb * a.nseg, PT, 0, st>>>(a);
   SS_LAUNCH_CHECK();
-  cudaGraphExec_t g;
-  int rc = get_graph(K, nb, jacobi, &g);
-  if (rc) return rc;
-  const int per_graph_launches = 5 * K->ticks_per_graph;
   // tick bound: every mode finishes within maxiter inner ticks + 2 ticks per cycle
   const int64_t max_ticks = maxiter + 3 * (maxiter / std::max<int64_t>(1, std::min<int64_t>(a.restart, maxiter + 1)) + 2) + 16;
   int64_t ticks = 0;
+  cudaGraphExec_t g;
+  int rc = SS_OK;
+  if (K->device_loop) {
+    rc = get_while_graph(K, nb, jacobi, &g);
+    if (rc) K->device_loop = 0;   // fall back to the host-polled loop
+  }
+  if (K->device_loop) {
+    long long lp[2] = {0, (long long)max_ticks + 2 * K->ticks_per_graph};
+    SS_CUDA(cudaMemcpyAsync(a.loop, lp, sizeof(lp), cudaMemcpyHostToDevice, st));
+    SS_CUDA(cudaGraphLaunch(g, st));
+    SS_CUDA(cudaMemcpyAsync(lp, a.loop, sizeof(lp), cudaMemcpyDeviceToHost, st));
+    SS_CUDA(cudaStreamSynchronize(st));
+    ticks = lp[0];
+    ss_count_launch((ticks / K->ticks_per_graph) * (5 * K->ticks_per_graph + 1));
+    int done = 0;
+    SS_CUDA(cudaMemcpy(&done, a.n_done, sizeof(int), cudaMemcpyDeviceToHost));
+    if (done < nb) {
+      ss_set_error("GMRES tick bound exceeded (internal state machine error)");
+      return SS_ERR_STATE;
+    }
+  }
+  rc = K->device_loop ? SS_OK : get_graph(K, nb, jacobi, &g);
+  if (rc) return rc;
+  const int per_graph_launches = 5 * K->ticks_per_graph;
   int it = 0;
-  bool finished = false;
+  bool finished = K->device_loop != 0;
   while (!finished) {
     SS_CUDA(cudaGraphLaunch(g, st));
     ss_count_launch(per_graph_launches);
@@ -1039,7 +1152,7 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
     }
     ++it;
   }
-  SS_CUDA(cudaEventSynchronize(K->ev[(it - 1) & 1]));
+  if (it > 0) SS_CUDA(cudaEventSynchronize(K->ev[(it - 1) & 1]));
   k_finalize<<<dim3(64, nb), 256, 0, st>>>(a);
   SS_LAUNCH_CHECK();
   if (x_dev)
