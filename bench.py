@@ -307,6 +307,18 @@ def run_b200(args):
     prof = ws.profile(omegas, TOL, BUDGET, jacobi=True)
     dom_name = max((k for k in prof if k != "spmv"), key=lambda k: prof[k]["ms"])
     dom = prof[dom_name]
+    traffic = None
+    try:   # DRAM traffic of the same kernel from the committed `ncu --set full` capture (J = 100 launch)
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_full.json")) as fh:
+            cap = json.load(fh)
+        rec = next(r for r in cap["launches"] if r["kernel"].startswith("void k_pass<2>"))
+        alg = nb * (100 + 2) * 16 * op.n
+        traffic = {"bytes_per_launch": rec["dram_read_bytes"] + rec["dram_write_bytes"],
+                   "algorithmic_bytes_same_launch": alg,
+                   "ratio": (rec["dram_read_bytes"] + rec["dram_write_bytes"]) / alg,
+                   "source": "profiles/r1_ncu_full.json (k_pass<2>, tick 100: J = 100)"}
+    except Exception:
+        traffic = None
     achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
     share = dom["ms"] / sum(v["ms"] for v in prof.values())
     passes_bytes = sum(prof[k]["bytes"] for k in prof if k != "spmv")
@@ -378,7 +390,7 @@ def run_b200(args):
                            "basis": "PROJECTION ONLY: value / 2e5 iterations per mode (krylov.py maxiter default; "
                                     "c2 needs >= 1e5 at 1e-10, SURVEY.md 8d)"}},
             "roofline": {"bound": "hbm", "kernel": f"k_pass<{dom_name}>", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "peak_kind": peak_kind, "share_of_step": share,
                          "all_basis_passes_gbs": passes_bytes / (passes_ms * 1e-3) / 1e9,
                          "per_kernel": prof},
