@@ -390,7 +390,10 @@ def run_b200(args):
                            "basis": "PROJECTION ONLY: value / 2e5 iterations per mode (krylov.py maxiter default; "
                                     "c2 needs >= 1e5 at 1e-10, SURVEY.md 8d)"}},
             "roofline": {"bound": "hbm", "kernel": f"k_pass<{dom_name}>", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                         "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": None if traffic is None else traffic["ratio"] * dom["bytes"] / dom["launches"],
+                         "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
+                         "traffic_detail": traffic,
                          "peak_kind": peak_kind, "share_of_step": share,
                          "all_basis_passes_gbs": passes_bytes / (passes_ms * 1e-3) / 1e9,
                          "per_kernel": prof},
