@@ -74,6 +74,7 @@ struct KArgs {
   double* hist;                // [b][hist_cap]
   unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
   long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap
+  int x_in_a;                  // cycle-end x update inside the next tick's pass-A launch (1) or own launch (0)
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -575,10 +576,20 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   const int b = blockIdx.x % a.nb, s = blockIdx.x / a.nb;
   ModeCtl* c = a.ctl + b;
   const int phase = c->phase;
+  const int tid = threadIdx.x;
+  if (PASS == PASS_A && phase == PH_XUPDATE && a.x_in_a) {
+    // cycle-end x += Q y rides on the next tick's pass-A launch (one launch per tick saved)
+    const int kx = c->k;
+    for (int j = tid; j < kx; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
+    __syncthreads();
+    stream_segment<PASS_X, 1>(a, b, s, kx, kx, coef, smem, mbar, red, nullptr);
+    if (!last_cta(a, b, PASS_X, a.nseg, &sflag)) return;
+    if (tid == 0) c->phase = PH_RESID;
+    return;
+  }
   if (PASS == PASS_X ? phase != PH_XUPDATE : phase != PH_INNER) return;
   const int k = c->k;
   const int J = PASS == PASS_X ? k : k + 1;
-  const int tid = threadIdx.x;
   double* qs = a.qs + (size_t)b * a.jcap;
   // coefficients of the update (qs folded in): B: qs_j c_j, C: qs_j c2_j, X: y_j (already scaled)
   if (PASS == PASS_B || PASS == PASS_C) {
@@ -884,6 +895,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   SS_CUDA(setattr((const void*)k_pass<PASS_X>));
   K->ticks_per_graph = n < 200000 ? 16 : 2;
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
+  K->a.x_in_a = 1;
+  if (const char* e = getenv("SS_X_IN_A")) K->a.x_in_a = atoi(e);
   if (const char* e = getenv("SS_TICKS_PER_GRAPH")) K->ticks_per_graph = std::max(1, atoi(e));
   return SS_OK;
 }
@@ -987,8 +1000,10 @@ static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
   SS_LAUNCH_CHECK();
   k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
   SS_LAUNCH_CHECK();
-  k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
-  SS_LAUNCH_CHECK();
+  if (!a.x_in_a) {
+    k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
+    SS_LAUNCH_CHECK();
+  }
   return SS_OK;
 }
 
@@ -1123,7 +1138,7 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
     SS_CUDA(cudaMemcpyAsync(lp, a.loop, sizeof(lp), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaStreamSynchronize(st));
     ticks = lp[0];
-    ss_count_launch((ticks / K->ticks_per_graph) * (5 * K->ticks_per_graph + 1));
+    ss_count_launch((ticks / K->ticks_per_graph) * ((a.x_in_a ? 4 : 5) * K->ticks_per_graph + 1));
     int done = 0;
     SS_CUDA(cudaMemcpy(&done, a.n_done, sizeof(int), cudaMemcpyDeviceToHost));
     if (done < nb) {
@@ -1133,7 +1148,7 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
   }
   rc = K->device_loop ? SS_OK : get_graph(K, nb, jacobi, &g);
   if (rc) return rc;
-  const int per_graph_launches = 5 * K->ticks_per_graph;
+  const int per_graph_launches = (a.x_in_a ? 4 : 5) * K->ticks_per_graph;
   int it = 0;
   bool finished = K->device_loop != 0;
   while (!finished) {
@@ -1310,8 +1325,10 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
     k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[4], st));
-    k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
-    SS_LAUNCH_CHECK();
+    if (!a.x_in_a) {
+      k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
+      SS_LAUNCH_CHECK();
+    }
     SS_CUDA(cudaEventRecord(ev[5], st));
     SS_CUDA(cudaMemcpyAsync(K->h_done, a.n_done, sizeof(int), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaEventSynchronize(ev[5]));
