@@ -16,6 +16,9 @@ from .errors import DeviceError, MeshError
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libss_b200.so"
+# A/B tooling only (tools/build_variant.py): load a differently built copy of the same library.
+if os.environ.get("SS_B200_LIB"):
+    LIB_PATH = Path(os.environ["SS_B200_LIB"]).resolve()
 
 P = C.c_void_p
 I32 = C.c_int

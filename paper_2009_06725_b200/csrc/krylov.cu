@@ -21,6 +21,7 @@
 // which other modes share the batch: per-mode results are bitwise invariant under batching and
 // mode order (the reference's test_spectral.py:187-205 contract).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <map>
@@ -75,6 +76,7 @@ struct KArgs {
   unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
   long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap
   int x_in_a;                  // cycle-end x update inside the next tick's pass-A launch (1) or own launch (0)
+  int gthr[3];                 // pass B: largest J using 1, 2, 4 warps per row block (8 above)
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -566,11 +568,132 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   }
 }
 
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Pass B for small J (J <= gthr[2]): G = 1, 2 or 4 warps share a 32-row block (thread (wg, lane)
+// owns row `lane`, columns j = wg + G*t) and the CTA's 8/G warp groups work on different blocks
+// of a chunk at once.  With G = 8 (stream_segment) every block is a CTA-wide step, which leaves
+// small-J chunks latency-bound; here a group needs only its own named barrier (none for G = 1).
+// Same two phases as stream_segment<PASS_B>: w -= sum_j q_j c_j, then acc_t += conj(q_j) w, with
+// the block's basis values held in registers between them.
+template <int G, int T>
+__device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, int J, const double2* coef,
+                                                  double2* smem, uint64_t* mbar, double2* red, double2* part) {
+  constexpr int NG = 8 / G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / G, wg = warp % G;
+  const int segb = a.seg_rows / RB;
+  const int blk_begin = s * segb;
+  const int blk_end = min(blk_begin + segb, a.nblk);
+  const int nblocks = blk_end - blk_begin;
+  const int belem = J * RB;
+  const int blk_elems = belem + RB;
+  // chunks of NG blocks (one per group), up to PASS_MAX_STAGES of them in the ring
+  const int CB = min(NG, nblocks);
+  const int stage_elems = CB * blk_elems;
+  const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
+  const int nchunks = (nblocks + CB - 1) / CB;
+  double2* vec = a.W + (size_t)b * a.ld;
+  auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
+  auto load_chunk = [&](int ci) {   // single producer thread
+    double2* st = stage(ci);
+    const int c0 = blk_begin + ci * CB;
+    const int nc = min(CB, blk_end - c0);
+    uint64_t* bar = &mbar[ci % NS];
+    mbar_expect_tx(bar, (unsigned)(nc * blk_elems * 16));
+    for (int c = 0; c < nc; ++c) bulk_g2s(st + c * belem, qblock(a, b, c0 + c), (unsigned)belem * 16u, bar);
+    bulk_g2s(st + CB * belem, vec + (size_t)c0 * RB, (unsigned)(nc * RB * 16), bar);
+  };
+  if (tid < PASS_MAX_STAGES) mbar_init(&mbar[tid], 1);
+  fence_mbar_init();
+  __syncthreads();
+  if (tid == 0)
+    for (int ci = 0; ci < NS - 1 && ci < nchunks; ++ci) load_chunk(ci);
+  double2 acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
+  int bi = 0;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    if (tid == 0 && ci + NS - 1 < nchunks) load_chunk(ci + NS - 1);   // stage of chunk ci-1 (released)
+    mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
+    const double2* st = stage(ci);
+    const int c0 = blk_begin + ci * CB;
+    const int nc = min(CB, blk_end - c0);
+    const double2* Vb = st + CB * belem;
+    if (grp < nc) {
+      const int c = grp;
+      const double2* S = st + c * belem + lane;
+      double2 qv[T];
+      double2 p = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int j = wg + G * t;
+        if (j < J) {
+          qv[t] = S[j * RB];
+          const double2 cf = coef[j];
+          p.x += qv[t].x * cf.x - qv[t].y * cf.y;
+          p.y += qv[t].x * cf.y + qv[t].y * cf.x;
+        } else {
+          qv[t] = make_double2(0.0, 0.0);
+        }
+      }
+      const int64_t row = (int64_t)(c0 + c) * RB + lane;
+      double2 v;
+      if (G == 1) {
+        v = csub(Vb[c * RB + lane], p);
+        vec[row] = v;
+      } else {
+        double2* rb = red + (bi & 1) * PT + grp * G * 32;   // group slot, double-buffered
+        rb[wg * 32 + lane] = p;
+        group_sync(1 + grp, 32 * G);
+        if (wg == 0) {
+          double2 tot = p;
+#pragma unroll
+          for (int w = 1; w < G; ++w) tot = cadd(tot, rb[w * 32 + lane]);
+          v = csub(Vb[c * RB + lane], tot);
+          vec[row] = v;
+          rb[lane] = v;
+        }
+        group_sync(1 + grp, 32 * G);
+        v = rb[lane];
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        acc[t].x += qv[t].x * v.x + qv[t].y * v.y;
+        acc[t].y += qv[t].x * v.y - qv[t].y * v.x;
+      }
+      ++bi;
+    }
+    fence_proxy_async();
+    __syncthreads();
+  }
+  if (tid == 0 && blk_begin * RB < a.n) {
+    const int64_t real_rows = min((int64_t)blk_end * RB, (int64_t)a.n) - (int64_t)blk_begin * RB;
+    atomicAdd(a.bytes + PASS_B, (unsigned long long)((J + 2) * real_rows * 16));
+  }
+  // rows -> lanes (warp sums), then groups in fixed order
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int j = wg + G * t;
+    const double x = warp_sum(acc[t].x), y = warp_sum(acc[t].y);
+    if (lane == 0 && j < J) red[grp * J + j] = make_double2(x, y);
+  }
+  __syncthreads();
+  for (int j = tid; j < J; j += PT) {
+    double2 tot = red[j];
+#pragma unroll
+    for (int g = 1; g < NG; ++g) tot = cadd(tot, red[g * J + j]);
+    part[j] = tot;
+  }
+}
+
 template <int PASS>
 __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   extern __shared__ __align__(128) double2 smem[];
   __shared__ double2 coef[256];
-  __shared__ double2 red[PT];
+  __shared__ double2 red[PASS == PASS_B ? 2 * PT : PT];
   __shared__ __align__(8) uint64_t mbar[PASS_MAX_STAGES];
   __shared__ int sflag;
   const int b = blockIdx.x % a.nb, s = blockIdx.x / a.nb;
@@ -601,7 +724,17 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   __syncthreads();
   double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
   const int T = (J + 7) / 8;
-  if (PASS == PASS_A || PASS == PASS_B) {
+  if (PASS == PASS_B && J <= a.gthr[2]) {
+    if (J <= a.gthr[0]) {
+      if (J <= 4) stream_segment_bg<1, 4>(a, b, s, J, coef, smem, mbar, red, part);
+      else if (J <= 8) stream_segment_bg<1, 8>(a, b, s, J, coef, smem, mbar, red, part);
+      else stream_segment_bg<1, 16>(a, b, s, J, coef, smem, mbar, red, part);
+    } else if (J <= a.gthr[1]) {
+      stream_segment_bg<2, 16>(a, b, s, J, coef, smem, mbar, red, part);
+    } else {
+      stream_segment_bg<4, 16>(a, b, s, J, coef, smem, mbar, red, part);
+    }
+  } else if (PASS == PASS_A || PASS == PASS_B) {
     if (T <= 2) stream_segment<PASS, 2>(a, b, s, J, k, coef, smem, mbar, red, part);
     else if (T <= 4) stream_segment<PASS, 4>(a, b, s, J, k, coef, smem, mbar, red, part);
     else if (T <= 8) stream_segment<PASS, 8>(a, b, s, J, k, coef, smem, mbar, red, part);
@@ -896,6 +1029,14 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   K->ticks_per_graph = n < 200000 ? 16 : 2;
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
   K->a.x_in_a = 1;
+  K->a.gthr[0] = 16;
+  K->a.gthr[1] = 32;
+  K->a.gthr[2] = 64;
+  if (const char* e = getenv("SS_PASS_G")) sscanf(e, "%d,%d,%d", &K->a.gthr[0], &K->a.gthr[1], &K->a.gthr[2]);
+  // T <= 16 columns per thread below G = 8 (register budget)
+  K->a.gthr[0] = std::min(K->a.gthr[0], 16);
+  K->a.gthr[1] = std::min(K->a.gthr[1], 32);
+  K->a.gthr[2] = std::min(K->a.gthr[2], 64);
   if (const char* e = getenv("SS_X_IN_A")) K->a.x_in_a = atoi(e);
   if (const char* e = getenv("SS_TICKS_PER_GRAPH")) K->ticks_per_graph = std::max(1, atoi(e));
   return SS_OK;
@@ -1211,14 +1352,32 @@ extern "C" int ss_krylov_history(const ss_krylov* K, int mode, int64_t count, do
   return SS_OK;
 }
 
-// One isolated basis pass (bench / profiling): runs k_pass<PASS_B> for nb modes, all forced into
-// phase INNER at basis index k (J = k+1 vectors).  Returns algorithmic bytes in *bytes.
+// One isolated basis pass (bench / profiling): runs k_pass<which> (A, B or C) for nb modes, all
+// forced into phase INNER at basis index k (J = k+1 vectors).  Returns algorithmic bytes in *bytes.
 __global__ void k_force_inner(KArgs a, int k) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.nb) return;
   a.ctl[b].phase = PH_INNER;
   a.ctl[b].k = k;
+  a.ctl[b].maxiter = 0x7fffffff;
+  a.ctl[b].iters = 0;
+  a.ctl[b].target = -1.0;
+  a.ctl[b].beta = 1.0;
   for (int j = 0; j <= k; ++j) a.qs[b * a.jcap + j] = 1.0;
+}
+
+// Bench input: w = 1 on the active rows (so ||w|| > 0 in pass C), zero projection coefficients.
+__global__ void k_bench_fill(KArgs a) {
+  const int64_t total = (int64_t)a.nb * a.ld;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i % a.ld;
+    a.W[i] = make_double2(row < a.n ? 1.0 : 0.0, 0.0);
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)a.nb * a.jcap;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    a.C1[i] = make_double2(0.0, 0.0);
+    a.C2[i] = make_double2(0.0, 0.0);
+  }
 }
 
 extern "C" int ss_krylov_bench_pass(ss_krylov* K, int nb, int k, int which, int reps, void* stream_, float* ms,
@@ -1233,15 +1392,23 @@ extern "C" int ss_krylov_bench_pass(ss_krylov* K, int nb, int k, int which, int 
   SS_CUDA(cudaEventCreate(&e0));
   SS_CUDA(cudaEventCreate(&e1));
   const unsigned gs = (unsigned)(nb * a.nseg);
-  // warm-up
-  if (which == PASS_A) k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
-  else k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+  k_bench_fill<<<4 * 148, 256, 0, st>>>(a);
   SS_LAUNCH_CHECK();
+  auto one = [&]() {
+    if (which == PASS_A) k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+    else if (which == PASS_B) k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+    else k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
+  };
+  // warm-up
+  one();
+  SS_LAUNCH_CHECK();
+  if (which == PASS_C) k_force_inner<<<(nb + 127) / 128, 128, 0, st>>>(a, k);
   SS_CUDA(cudaEventRecord(e0, st));
   for (int r = 0; r < reps; ++r) {
-    if (which == PASS_A) k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
-    else k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+    one();
     SS_LAUNCH_CHECK();
+    // pass C advances k (Givens step): re-arm (a ~2 us kernel, included in the time)
+    if (which == PASS_C) k_force_inner<<<(nb + 127) / 128, 128, 0, st>>>(a, k);
   }
   SS_CUDA(cudaEventRecord(e1, st));
   SS_CUDA(cudaEventSynchronize(e1));
@@ -1250,7 +1417,7 @@ extern "C" int ss_krylov_bench_pass(ss_krylov* K, int nb, int k, int which, int 
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   const int64_t J = k + 1;
-  // A: read Q (J vectors) + w;  B: read Q + w, write w
+  // A: read Q (J vectors) + w;  B: read Q + w, write w;  C: read Q + w, write q_{k+1}
   *bytes = (int64_t)nb * 16 * a.n * (J + (which == PASS_A ? 1 : 2));
   return SS_OK;
 }
@@ -1332,12 +1499,15 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
     SS_CUDA(cudaEventRecord(ev[5], st));
     SS_CUDA(cudaMemcpyAsync(K->h_done, a.n_done, sizeof(int), cudaMemcpyDeviceToHost, st));
     SS_CUDA(cudaEventSynchronize(ev[5]));
+    static FILE* dump = getenv("SS_PROFILE_DUMP") ? fopen(getenv("SS_PROFILE_DUMP"), "w") : nullptr;
     for (int q = 0; q < 5; ++q) {
       float ms = 0;
       SS_CUDA(cudaEventElapsedTime(&ms, ev[q], ev[q + 1]));
       ms_out[q] += ms;
       launches_out[q] += 1;
+      if (dump) fprintf(dump, q < 4 ? "%.4f," : "%.4f\n", ms);
     }
+    if (dump) fflush(dump);
     ++tick;
     done = K->h_done[0];
     if (done >= a.nb) break;

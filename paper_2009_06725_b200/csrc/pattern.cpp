@@ -7,7 +7,10 @@
 // (COO->CSR, kron, bmat and fancy indexing all keep them).  Values are not
 // computed here: the device element kernel (assemble.cu) fills them through the element maps.
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -16,6 +19,7 @@
 
 #include "ss_common.h"
 #include "ss_pattern.h"
+#include "ss_spmv.cuh"
 
 static std::mutex g_err_mu;
 static std::string g_err;
@@ -192,6 +196,58 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
   }
   nodes_rows.clear(); vert_rows.clear(); prow_nodes.clear();
 
+  // SpMV row schedule (block -> rows).  Default: natural order (the GMRES tick measured fastest,
+  // pass C having just written P in that order).  SS_SPMV_SCHED=1: anchor schedule --
+  // anchor(node) = smallest vertex of any element containing it (the generators number vertices
+  // coherently in space, so rows with close anchors share columns); rows sorted by anchor are cut
+  // into the saddle block count with balanced gather work, velocity rows first inside a block
+  // (3% faster standalone SpMV, 2% slower inside the tick).  Results never depend on it: every
+  // (row, mode) sum is still formed by one thread in CSR order.
+  {
+    std::vector<int> anchor(n_vel_nodes, INT32_MAX);
+    for (int64_t e = 0; e < n_elements; ++e) {
+      int mv = INT32_MAX;
+      for (int a = 0; a < nvloc; ++a) mv = std::min(mv, (int)vel_conn[e * nloc + a]);
+      for (int a = 0; a < nloc; ++a) {
+        int& an = anchor[vel_conn[e * nloc + a]];
+        an = std::min(an, mv);
+      }
+    }
+    const int nitems = nfree + npf;
+    std::vector<int64_t> key(nitems);
+    for (int r = 0; r < nfree; ++r) key[r] = ((int64_t)anchor[P->free_nodes[r]] << 32) | (int64_t)r;
+    for (int j = 0; j < npf; ++j) key[nfree + j] = ((int64_t)anchor[P->pres_of_row[j]] << 32) | (int64_t)(nfree + j);
+    std::sort(key.begin(), key.end());
+    std::vector<int> items(nitems);
+    std::vector<double> wsum(nitems + 1, 0.0);
+    for (int i = 0; i < nitems; ++i) {
+      const int it = (int)(key[i] & 0xffffffff);
+      items[i] = it;
+      const double w = it < nfree ? (double)dim * (P->nptr[it + 1] - P->nptr[it]) + (P->pptr[it + 1] - P->pptr[it])
+                                  : (double)dim * (P->tptr[it - nfree + 1] - P->tptr[it - nfree]);
+      wsum[i + 1] = wsum[i] + w + 4.0;   // + per-row overhead
+    }
+    const int nsb = saddle_nsb_host(nfree, npf);
+    P->sbptr.assign(nsb + 1, nitems);
+    P->sbptr[0] = 0;
+    int i = 0;
+    for (int b = 1; b < nsb; ++b) {
+      const double target = wsum[nitems] * b / nsb;
+      while (i < nitems && wsum[i] < target) ++i;
+      P->sbptr[b] = i;
+    }
+    for (int b = 0; b < nsb; ++b) std::sort(items.begin() + P->sbptr[b], items.begin() + P->sbptr[b + 1]);
+    const char* sched = getenv("SS_SPMV_SCHED");
+    if (!sched || atoi(sched) == 0) {   // default, natural order: 128 node rows / 32 pressure rows per block
+      for (int q = 0; q < nitems; ++q) items[q] = q;
+      const int nvb = (nfree + SPMV_VROWS - 1) / SPMV_VROWS;
+      for (int b = 0; b < nsb; ++b)
+        P->sbptr[b] = b < nvb ? b * SPMV_VROWS : std::min(nfree + (b - nvb) * SPMV_PROWS, nitems);
+      P->sbptr[nsb] = nitems;
+    }
+    P->sitems = items;
+  }
+
   // Constrained rows a_full[fixed_idx] (assembly.py:471-476,491): rows of fixed velocity nodes
   // (all node / vertex neighbours, global ids) and, if the pressure is pinned, the row of vertex 0.
   {
@@ -320,6 +376,7 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
   UP(P->lptr, lptr); UP(P->lcol, lcol); UP(P->ltptr, ltptr); UP(P->ltcol, ltcol);
   UP(P->free_nodes, free_nodes); UP(P->rank, node_rank); UP(P->pres_of_row, pres_of_row);
   UP(P->vert_pdof, vert_pdof);
+  UP(P->sitems, sitems); UP(P->sbptr, sbptr);
 #undef UP
   if ((rc = upload(P, conn32, &P->d_conn))) { delete P; return rc; }
   if ((rc = upload(P, P->emap, &P->d_emap))) { delete P; return rc; }

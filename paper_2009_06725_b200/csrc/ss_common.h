@@ -66,6 +66,10 @@ struct SsOperatorDev {
   const int* node_rank;    // node -> rank or -1
   const int* pres_of_row;  // pressure dof j -> vertex
   const int* vert_pdof;    // vertex -> pressure dof (0..npf-1) or -1
+  // Locality schedule of the mode-interleaved SpMV: block b processes rows sitems[sbptr[b] ..
+  // sbptr[b+1]) (velocity node rank r, or nfree + pressure dof), rows grouped by anchor vertex so
+  // that concurrently running blocks gather from one compact window of x.
+  const int* sitems; const int* sbptr;
 };
 
 // Generic complex CSR operator (drop-in gmres(matrix, rhs) on arbitrary matrices).

@@ -18,6 +18,7 @@ struct ss_pattern {
   std::vector<int> emap, color_ptr, color_elems;
   // constrained rows (fixed velocity nodes; pinned pressure row)
   std::vector<int> fixed_nodes, frank, xptr, xcol, xpptr, xpcol, pincol;
+  std::vector<int> sitems, sbptr;   // SpMV locality schedule (ss_common.h SsOperatorDev)
   double2* d_xsm = nullptr;
   double* d_xdp = nullptr;
   double* d_pinv = nullptr;

@@ -241,13 +241,12 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
                                                          int nb, int ps, const double2* __restrict__ x,
                                                          double2* __restrict__ y, int64_t ld, int jacobi,
                                                          Active active, Omega omega_of, Scale scale_of) {
-  const int nvb = saddle_nvb(op);
-  const bool vel = blk < nvb;
-  const int r0 = vel ? blk * SPMV_VROWS : (blk - nvb) * SPMV_PROWS;
-  const int rend = vel ? min(r0 + SPMV_VROWS, op.nfree) : min(r0 + SPMV_PROWS, op.npf);
-  const int npairs = (rend - r0) * nb;
+  const int i0 = __ldg(op.sbptr + blk), i1 = __ldg(op.sbptr + blk + 1);
+  const int npairs = (i1 - i0) * nb;
   for (int pr = sub * blockDim.x + threadIdx.x; pr < npairs; pr += split * blockDim.x) {
-    const int r = r0 + pr / nb, m = pr % nb;
+    const int item = __ldg(op.sitems + i0 + pr / nb), m = pr % nb;
+    const bool vel = item < op.nfree;
+    const int r = vel ? item : item - op.nfree;
     if (!active(m)) continue;
     const double om = omega_of(m), xs = scale_of(m);
     const double2* P = x + m;
