@@ -259,8 +259,8 @@ __device__ __forceinline__ void spmv_inner_csr_mode(const KArgs& a, int b, int s
 }
 
 // Cycle-boundary decisions of mode b once every CTA has contributed (krylov.py:93-103,155-162).
-__device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int phase, int* sflag) {
-  if (!last_cta(a, b, 0, a.nsb * a.spmv_split, sflag)) return;
+// Called by the last CTA of the tick SpMV for every mode it touched.
+__device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int phase) {
   ModeCtl* c = a.ctl + b;
   if (phase != PH_RESID) {
     if (threadIdx.x == 0 && phase == PH_START) c->phase = PH_INNER;
@@ -342,9 +342,12 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   if (sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
     for (int b = 0; b < a.nb; ++b)
       if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
+  // one election for the whole batch (slot 6 of mode 0's counters): the last CTA to finish makes
+  // every mode's cycle decisions
+  if (!last_cta(a, 0, 6, (int)gridDim.x, &sflag)) return;
   for (int b = 0; b < a.nb; ++b) {
     const int ph = sph[b];
-    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph, &sflag);
+    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
   }
 }
 
@@ -1052,7 +1055,11 @@ extern "C" int ss_krylov_create_saddle(const ss_pattern* P, int max_batch, int r
   K->a.kind = 0;
   K->a.op = P->op;
   K->a.nsb = saddle_nsb_host(P->nfree, P->npf);
-  K->a.spmv_split = std::max(1, std::min(16, (8 * 148 + K->a.nsb - 1) / K->a.nsb));
+  // sub-CTAs per SpMV row block when there are few blocks: about two (row, mode) pairs of a
+  // 128-row block per thread, and no more than needed to fill the GPU (config 1: 9)
+  K->a.spmv_split = std::max(1, std::min(std::min(16, (8 * 148 + K->a.nsb - 1) / K->a.nsb),
+                                         (SPMV_VROWS * max_batch + PT / 2 - 1) / (PT / 2)));
+  if (const char* e = getenv("SS_SPMV_SPLIT")) K->a.spmv_split = std::max(1, atoi(e));
   int rc = krylov_common_init(K, P->op.n, max_batch, restart, hist_cap);
   if (!rc) rc = kalloc(K, (size_t)max_batch * K->a.nsb, &K->a.spart);
   if (rc) { delete K; return rc; }
