@@ -251,3 +251,22 @@ def test_batch_composition_and_order_bitwise(c1):
         assert np.array_equal(X[j], Xs.cpu().numpy()[0])
         assert np.array_equal(X[j], Xr[j])
         assert rep[j].iterations == reps[0].iterations
+
+
+@pytest.mark.gpu
+def test_maximum_restart_matches_oracle(c1):
+    """restart = MAX_RESTART (240): the widest basis-pass instantiations (J up to 241 vectors,
+    32 columns per thread, one-stage ring) and the largest triangular solve, checked against the
+    oracle's CGS2 GMRES on the same matrix over one full restart cycle plus a few iterations."""
+    from oracle import scvs
+    from paper_2009_06725_b200.krylov import MAX_RESTART
+
+    case, props, _ = c1
+    s = assemble_mode_system(case.qmesh, props, case.omegas[2], h_mode=case.h_modes()[2])
+    budget = MAX_RESTART + 10
+    x, rep = gmres_solve(s, SolverSettings(tolerance=C1_TOL, restart=MAX_RESTART, max_iterations=budget))
+    a = s.matrix
+    xo, it, hist, _ = scvs.gmres(a, s.rhs, C1_TOL, MAX_RESTART, budget, scvs.jacobi_scale(a))
+    assert rep.iterations == it == budget
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=1e-6)
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
