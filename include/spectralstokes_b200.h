@@ -100,6 +100,13 @@ int ss_residual_norms(const ss_pattern* p, int nb, const double* omegas_dev, con
 /* L2(Omega) norms of nb nodal velocity-space fields (nb x n_vel_nodes x ncomp complex) by element
  * quadrature (metrics.l2_norm, metrics.py:12-18; interpolate_at_quadrature, assembly.py:497-511). */
 int ss_l2_norms(const ss_pattern* p, int nb, int ncomp, const double* fields_dev, double* out_host, void* stream);
+/* Points of the degree-4 element rule of reference_shapes(dim) (assembly.py:51-86): 6 (2D), 11 (3D). */
+int ss_quadrature_points(int dim, int* nq);
+/* Nodal velocity-space field (n_vel_nodes x ncomp complex) -> quadrature coordinates (ne x nq x dim),
+ * values (ne x nq x ncomp complex) and Jacobian-weighted weights (ne x nq), all device buffers
+ * (interpolate_at_quadrature, assembly.py:497-511; used by metrics.field_error, metrics.py:21-39). */
+int ss_interp_quadrature(const ss_pattern* p, int ncomp, const double* nodal_dev, double* coords_dev,
+                         double* vals_dev, double* w_dev, void* stream);
 /* Jacobi scale vectors 1/diag (1 where diag = 0) per mode (jacobi_precondition, krylov.py:49-60). */
 int ss_jacobi(const ss_pattern* p, int nb, const double* omegas_dev, double* scale_dev, int64_t ld, void* stream);
 /* Reduced solutions -> nodal velocity (nb x n_vel_nodes*dim) and pressure (nb x n_vertices),

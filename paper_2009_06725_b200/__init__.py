@@ -28,7 +28,15 @@ from .mesh import (  # noqa: F401
     QuadraticMesh,
     promote_to_quadratic,
 )
-from .metrics import l2_norm, l2_norms  # noqa: F401
+from .metrics import (  # noqa: F401
+    field_error,
+    fit_loglog_slope,
+    flow_rate,
+    interpolate_at_quadrature,
+    l2_norm,
+    l2_norms,
+    patch_area,
+)
 from .spectral import (  # noqa: F401
     BoundaryWaveform,
     adaptive_mode_refinement,

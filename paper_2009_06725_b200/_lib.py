@@ -54,6 +54,8 @@ SIGNATURES = {
     "ss_residual_norms": (I32, [P, I32, P, P, P, I64, PD, P]),
     "ss_expand": (I32, [P, I32, P, I64, P, P, P, P]),
     "ss_l2_norms": (I32, [P, I32, I32, P, PD, P]),
+    "ss_quadrature_points": (I32, [I32, C.POINTER(C.c_int)]),
+    "ss_interp_quadrature": (I32, [P, I32, P, P, P, P, P]),
     "ss_krylov_create_saddle": (I32, [P, I32, I32, I64, C.POINTER(P)]),
     "ss_krylov_create_csr": (I32, [I32, I32, I64, PI32, PI32, I32, PD, PD, I32, I32, I32, I64, C.POINTER(P)]),
     "ss_krylov_destroy": (None, [P]),

@@ -548,6 +548,7 @@ extern "C" int ss_residual_norms(const ss_pattern* P, int nb, const double* omeg
 // ------------------------------------------------------------------------------------------------
 __constant__ double c_qw[16];          // quadrature weights
 __constant__ double c_phi[16 * 10];    // P2 values at the quadrature points [q][a]
+__constant__ double c_lam[16 * 4];     // barycentric coordinates of the quadrature points [q][v]
 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_l2_partials(const int* __restrict__ conn, const double* __restrict__ vnodes,
@@ -600,13 +601,11 @@ __global__ void __launch_bounds__(256) k_l2_partials(const int* __restrict__ con
   if (threadIdx.x == 0) part[(size_t)b * gridDim.x + blockIdx.x] = red[0];
 }
 
-extern "C" int ss_l2_norms(const ss_pattern* P, int nb, int ncomp, const double* fields_dev, double* out_host,
-                           void* stream_) {
-  if (!P || nb < 1 || ncomp < 1 || !fields_dev || !out_host) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
-  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
-  cudaStream_t st = (cudaStream_t)stream_;
-  // degree-4 rule and P2 values at its points (same construction as reference_tables)
-  const int dim = P->dim, nl = dim == 2 ? 6 : 10;
+// Degree-4 element rule of reference_shapes (assembly.py:51-128, same point order), the P2 values
+// at its points [q][a] and the barycentric coordinates [q][v] (assembly.py:89-91), uploaded to
+// constant memory.  Returns the number of points.
+static int upload_quadrature(int dim, cudaStream_t st, int* nq_out) {
+  const int nl = dim == 2 ? 6 : 10;
   std::vector<std::vector<double>> bary;
   std::vector<double> w;
   if (dim == 2) {
@@ -654,8 +653,28 @@ extern "C" int ss_l2_norms(const ss_pattern* P, int nb, int ncomp, const double*
       phi[q * nl + dim + 1 + e] = 4.0 * L[i] * L[j];
     }
   }
+  std::vector<double> lam(nq * 4, 0.0);
+  for (int q = 0; q < nq; ++q) {
+    double sum = 0;
+    for (int c = 1; c <= dim; ++c) sum += bary[q][c];
+    lam[q * 4] = 1.0 - sum;
+    for (int c = 1; c <= dim; ++c) lam[q * 4 + c] = bary[q][c];
+  }
   SS_CUDA(cudaMemcpyToSymbolAsync(c_qw, w.data(), sizeof(double) * nq, 0, cudaMemcpyHostToDevice, st));
   SS_CUDA(cudaMemcpyToSymbolAsync(c_phi, phi.data(), sizeof(double) * nq * nl, 0, cudaMemcpyHostToDevice, st));
+  SS_CUDA(cudaMemcpyToSymbolAsync(c_lam, lam.data(), sizeof(double) * nq * 4, 0, cudaMemcpyHostToDevice, st));
+  *nq_out = nq;
+  return SS_OK;
+}
+
+extern "C" int ss_l2_norms(const ss_pattern* P, int nb, int ncomp, const double* fields_dev, double* out_host,
+                           void* stream_) {
+  if (!P || nb < 1 || ncomp < 1 || !fields_dev || !out_host) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int dim = P->dim;
+  int nq = 0;
+  if (int rc = upload_quadrature(dim, st, &nq)) return rc;
   const int nblk = (int)((P->ne + 255) / 256);
   double* part = nullptr;
   SS_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * nblk * nb, st));
@@ -674,5 +693,83 @@ extern "C" int ss_l2_norms(const ss_pattern* P, int nb, int ncomp, const double*
     for (int q = 0; q < nblk; ++q) acc += h[(size_t)b * nblk + q];
     out_host[b] = std::sqrt(acc);
   }
+  return SS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Nodal velocity-space field -> values at the element quadrature points (assembly.py:497-511):
+// coords[e][q][d] = sum_v lam[q][v] x_v,  vals[e][q][c] = sum_a phi[q][a] f[conn[e][a]][c],
+// w[e][q] = |det J_e| * weight_q.  One thread per element.
+// ------------------------------------------------------------------------------------------------
+template <int DIM>
+__global__ void __launch_bounds__(256) k_interp_quad(const int* __restrict__ conn, const double* __restrict__ vnodes,
+                                                     int64_t ne, int ncomp, int nq,
+                                                     const double2* __restrict__ f, double* __restrict__ coords,
+                                                     double2* __restrict__ vals, double* __restrict__ w) {
+  constexpr int NL = DIM == 2 ? 6 : 10, NV = DIM + 1;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int* c = conn + e * NL;
+  double x[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x[v][d] = vnodes[(size_t)c[v] * DIM + d];
+  double det;
+  if (DIM == 2) {
+    det = (x[1][0] - x[0][0]) * (x[2][1] - x[0][1]) - (x[2][0] - x[0][0]) * (x[1][1] - x[0][1]);
+  } else {
+    const double a0 = x[1][0] - x[0][0], a1 = x[1][1] - x[0][1], a2 = x[1][2] - x[0][2];
+    const double b0 = x[2][0] - x[0][0], b1 = x[2][1] - x[0][1], b2 = x[2][2] - x[0][2];
+    const double c0 = x[3][0] - x[0][0], c1 = x[3][1] - x[0][1], c2 = x[3][2] - x[0][2];
+    det = a0 * (b1 * c2 - b2 * c1) - b0 * (a1 * c2 - a2 * c1) + c0 * (a1 * b2 - a2 * b1);
+  }
+  for (int q = 0; q < nq; ++q) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double acc = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc += c_lam[q * 4 + v] * x[v][d];
+      coords[((size_t)e * nq + q) * DIM + d] = acc;
+    }
+    w[(size_t)e * nq + q] = fabs(det) * c_qw[q];
+  }
+  for (int comp = 0; comp < ncomp; ++comp) {
+    double2 u[NL];
+#pragma unroll
+    for (int a = 0; a < NL; ++a) u[a] = f[(size_t)c[a] * ncomp + comp];
+    for (int q = 0; q < nq; ++q) {
+      double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int a = 0; a < NL; ++a) {
+        v.x += c_phi[q * NL + a] * u[a].x;
+        v.y += c_phi[q * NL + a] * u[a].y;
+      }
+      vals[((size_t)e * nq + q) * ncomp + comp] = v;
+    }
+  }
+}
+
+extern "C" int ss_quadrature_points(int dim, int* nq) {
+  if ((dim != 2 && dim != 3) || !nq) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  *nq = dim == 2 ? 6 : 11;
+  return SS_OK;
+}
+
+extern "C" int ss_interp_quadrature(const ss_pattern* P, int ncomp, const double* nodal_dev, double* coords_dev,
+                                    double* vals_dev, double* w_dev, void* stream_) {
+  if (!P || ncomp < 1 || !nodal_dev || !coords_dev || !vals_dev || !w_dev) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)stream_;
+  int nq = 0;
+  if (int rc = upload_quadrature(P->dim, st, &nq)) return rc;
+  const unsigned grid = (unsigned)((P->ne + 255) / 256);
+  if (P->dim == 2)
+    k_interp_quad<2><<<grid, 256, 0, st>>>(P->d_conn, P->d_vnodes, P->ne, ncomp, nq, (const double2*)nodal_dev,
+                                            coords_dev, (double2*)vals_dev, w_dev);
+  else
+    k_interp_quad<3><<<grid, 256, 0, st>>>(P->d_conn, P->d_vnodes, P->ne, ncomp, nq, (const double2*)nodal_dev,
+                                            coords_dev, (double2*)vals_dev, w_dev);
+  SS_LAUNCH_CHECK();
   return SS_OK;
 }

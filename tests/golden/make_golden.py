@@ -19,6 +19,9 @@ Fixtures
   c2_pattern.npz  BASELINE config 2 (jittered 199 800-tet pipe): pattern hash, sampled A@x and rhs
   small3d.npz     down-scaled instances of the config 3/4/5 generators (bend, Y-junction, jittered
                   pipe), two modes each solved by the reference to 1e-10
+  post.npz        post-processing on seeded complex fields: interpolate_at_quadrature, l2_norm,
+                  field_error vs an analytic point oracle, flow_rate and patch_area of every
+                  boundary patch, fit_loglog_slope             (assembly.py:497-511, metrics.py:12-113)
 """
 
 from __future__ import annotations
@@ -45,6 +48,7 @@ sys.path.insert(0, str(REPO))
 
 from spectralstokes import assembly as RA  # noqa: E402
 from spectralstokes import krylov as RK  # noqa: E402
+from spectralstokes import metrics as RME  # noqa: E402
 from spectralstokes import mesh as RM  # noqa: E402
 from spectralstokes import spectral as RSP  # noqa: E402
 from spectralstokes import structured as RS  # noqa: E402
@@ -257,8 +261,49 @@ def make_c2_pattern():
     print("c2 pattern", time.perf_counter() - t0, "s")
 
 
+def post_oracle(xy):
+    """Analytic point field for field_error (shared with tests/test_*_post.py): complex, dim-vector."""
+    x = np.asarray(xy, dtype=float)
+    d = x.shape[1]
+    cols = [np.sin(1.3 * x[:, 0]) + 0.5j * x[:, 1] ** 2, np.cos(0.7 * x[:, 1]) - 0.25j * x[:, 0]]
+    if d == 3:
+        cols.append(x[:, 2] * x[:, 0] + 1j * np.sin(x[:, 2]))
+    return np.stack(cols, axis=1)
+
+
+def make_post():
+    out = {}
+    rng = np.random.default_rng(404)
+    for name, q in (("c1", _ref_qmesh(c1_case().mesh)),
+                    ("pipe3d", _ref_qmesh(pipe3d_case().mesh, "cylinder", pipe3d_case().radius))):
+        out.update(_mesh_arrays(name, q))
+        nvn, dim = q.n_velocity_nodes, q.dim
+        vec = rng.standard_normal((nvn, dim)) + 1j * rng.standard_normal((nvn, dim))
+        sca = rng.standard_normal(nvn)
+        # nodal interpolant of the analytic field (so field_error is small but non-zero)
+        near = post_oracle(q.nodes) + 1e-3 * vec
+        out[f"{name}_vec"], out[f"{name}_sca"], out[f"{name}_near"] = vec, sca, near
+        coords, vals, w = RA.interpolate_at_quadrature(q, vec)
+        out[f"{name}_iq_coords"], out[f"{name}_iq_vals"], out[f"{name}_iq_w"] = coords, vals, w
+        _, svals, _ = RA.interpolate_at_quadrature(q, sca)
+        out[f"{name}_iq_svals"] = svals
+        out[f"{name}_l2_vec"] = np.float64(RME.l2_norm(vec, q))
+        out[f"{name}_field_error"] = np.float64(RME.field_error(near, post_oracle, q))
+        for pn in sorted(q.boundary_patches):
+            if not q.boundary_patches[pn].faces.size:
+                continue
+            out[f"{name}_flow_{pn}"] = np.complex128(RME.flow_rate(vec, q, pn))
+            out[f"{name}_flowreal_{pn}"] = np.float64(RME.flow_rate(vec.real, q, pn))
+            out[f"{name}_area_{pn}"] = np.float64(RME.patch_area(q, pn))
+    xs = np.array([0.5, 0.25, 0.125, 0.0625])
+    ys = 3.0 * xs ** 2.1 * (1 + 0.01 * np.array([1, -1, 1, -1]))
+    out["fit_x"], out["fit_y"], out["fit_slope"] = xs, ys, np.float64(RME.fit_loglog_slope(xs, ys))
+    np.savez_compressed(HERE / "post.npz", **out)
+    print("post", {k: v for k, v in out.items() if "flow" in k or "area" in k or "error" in k})
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d"]
+    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d", "post"]
     with Pool(min(9, os.cpu_count() or 1)) as pool:
         if "shapes" in what:
             make_shapes()
@@ -272,3 +317,5 @@ if __name__ == "__main__":
             make_pipe3d(pool)
         if "small3d" in what:
             make_small3d(pool)
+        if "post" in what:
+            make_post()

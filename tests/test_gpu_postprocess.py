@@ -80,3 +80,35 @@ def test_adaptive_square_wave_differences_decrease(fluid):
     # the adaptive result equals solving the same modes directly
     ref = [np.sqrt(0.5 * wf.period) * oracle.l2_norm(s.velocity, q) for s in sols[1:] if s.omega != 0]
     np.testing.assert_allclose(diffs, ref, rtol=1e-12)
+
+
+def _post_oracle(xy):
+    """Same analytic point field as tests/golden/make_golden.py:post_oracle."""
+    x = np.asarray(xy, dtype=float)
+    cols = [np.sin(1.3 * x[:, 0]) + 0.5j * x[:, 1] ** 2, np.cos(0.7 * x[:, 1]) - 0.25j * x[:, 0]]
+    if x.shape[1] == 3:
+        cols.append(x[:, 2] * x[:, 0] + 1j * np.sin(x[:, 2]))
+    return np.stack(cols, axis=1)
+
+
+@pytest.mark.parametrize("name", ["c1", "pipe3d"])
+def test_interpolate_at_quadrature_and_field_error_match_reference(name):
+    """Device interpolation (assembly.py:497-511) and field_error / l2_norm (metrics.py:12-39)
+    against the reference's own outputs on the same meshes and seeded fields."""
+    from paper_2009_06725_b200 import field_error, interpolate_at_quadrature
+
+    g = golden("post.npz")
+    q = c1_case().qmesh if name == "c1" else pipe3d_case().qmesh
+    vec, sca = g[f"{name}_vec"], g[f"{name}_sca"]
+    coords, vals, w = interpolate_at_quadrature(q, vec)
+    assert coords.shape == g[f"{name}_iq_coords"].shape and vals.shape == g[f"{name}_iq_vals"].shape
+    np.testing.assert_allclose(coords, g[f"{name}_iq_coords"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(w, g[f"{name}_iq_w"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(vals, g[f"{name}_iq_vals"], rtol=0, atol=1e-13 * np.abs(vec).max())
+    _, svals, _ = interpolate_at_quadrature(q, sca)
+    assert not np.iscomplexobj(svals) and svals.shape == g[f"{name}_iq_svals"].shape
+    np.testing.assert_allclose(svals, g[f"{name}_iq_svals"], rtol=0, atol=1e-13 * np.abs(sca).max())
+    assert l2_norm(vec, q) == pytest.approx(float(g[f"{name}_l2_vec"]), rel=1e-12)
+    assert field_error(g[f"{name}_near"], _post_oracle, q) == pytest.approx(float(g[f"{name}_field_error"]), rel=1e-9)
+    with pytest.raises(ZeroDivisionError):
+        field_error(vec, lambda xy: np.zeros((len(xy), q.dim)), q)
