@@ -159,6 +159,20 @@ int ss_krylov_bench_pass(ss_krylov* k, int nb, int kidx, int which, int reps, vo
 int ss_reconstruct(int nb, int nt, int64_t n, const double* fields_dev, const double* phases_dev, double* out_dev,
                    void* stream);
 
+/* ---- Field snapshots (host runtime, io.py:88-183): "%.17g" text, byte-identical to the reference's
+ * "{:.17g}" writer, formatted/parsed in parallel.  Paths are NUL-terminated UTF-8. ---- */
+/* Native snapshot (io.py:104-114).  nodes/velocity: n_vel x dim, pressure: n_vert. */
+int ss_write_snapshot(const char* path, int dim, int64_t n_vel, int64_t n_vert, const double* nodes,
+                      const double* velocity, const double* pressure, double time);
+/* Legacy-VTK quadratic unstructured grid (write_vtk_snapshot, io.py:140-183); velocity / pressure
+ * may be NULL; mid-edge pressures from edges (n_vel - n_vert x 2). */
+int ss_write_vtk(const char* path, const char* title, int dim, int64_t n_vel, int64_t n_vert, const double* nodes,
+                 int64_t ne, int nloc, const int64_t* vel_conn, const int64_t* edges, const double* velocity,
+                 const double* pressure);
+/* Data blocks of a native snapshot whose header the caller parsed (read_field_snapshot, io.py:117-134). */
+int ss_read_snapshot(const char* path, int dim, int64_t n_vel, int64_t n_vert, double* coords, double* velocity,
+                     double* pressure);
+
 #ifdef __cplusplus
 }
 #endif

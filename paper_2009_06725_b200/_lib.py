@@ -55,6 +55,9 @@ SIGNATURES = {
     "ss_expand": (I32, [P, I32, P, I64, P, P, P, P]),
     "ss_l2_norms": (I32, [P, I32, I32, P, PD, P]),
     "ss_quadrature_points": (I32, [I32, C.POINTER(C.c_int)]),
+    "ss_write_snapshot": (I32, [C.c_char_p, I32, I64, I64, PD, PD, PD, D]),
+    "ss_write_vtk": (I32, [C.c_char_p, C.c_char_p, I32, I64, I64, PD, I64, I32, PI64, PI64, PD, PD]),
+    "ss_read_snapshot": (I32, [C.c_char_p, I32, I64, I64, PD, PD, PD]),
     "ss_interp_quadrature": (I32, [P, I32, P, P, P, P, P]),
     "ss_krylov_create_saddle": (I32, [P, I32, I32, I64, C.POINTER(P)]),
     "ss_krylov_create_csr": (I32, [I32, I32, I64, PI32, PI32, I32, PD, PD, I32, I32, I32, I64, C.POINTER(P)]),

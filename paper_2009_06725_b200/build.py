@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libss_b200.so"
-SOURCES = ["pattern.cpp", "assemble.cu", "krylov.cu", "reconstruct.cu"]
+SOURCES = ["pattern.cpp", "assemble.cu", "krylov.cu", "reconstruct.cu", "snapshot.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

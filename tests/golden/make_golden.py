@@ -19,6 +19,8 @@ Fixtures
   c2_pattern.npz  BASELINE config 2 (jittered 199 800-tet pipe): pattern hash, sampled A@x and rhs
   small3d.npz     down-scaled instances of the config 3/4/5 generators (bend, Y-junction, jittered
                   pipe), two modes each solved by the reference to 1e-10
+  snap.npz        field snapshots written by the reference (native text + legacy VTK, 2D and 3D)
+                  as raw bytes, with their inputs                              (io.py:88-183)
   post.npz        post-processing on seeded complex fields: interpolate_at_quadrature, l2_norm,
                   field_error vs an analytic point oracle, flow_rate and patch_area of every
                   boundary patch, fit_loglog_slope             (assembly.py:497-511, metrics.py:12-113)
@@ -48,6 +50,7 @@ sys.path.insert(0, str(REPO))
 
 from spectralstokes import assembly as RA  # noqa: E402
 from spectralstokes import krylov as RK  # noqa: E402
+from spectralstokes import io as RIO  # noqa: E402
 from spectralstokes import metrics as RME  # noqa: E402
 from spectralstokes import mesh as RM  # noqa: E402
 from spectralstokes import spectral as RSP  # noqa: E402
@@ -302,8 +305,36 @@ def make_post():
     print("post", {k: v for k, v in out.items() if "flow" in k or "area" in k or "error" in k})
 
 
+def make_snapshots():
+    import tempfile
+
+    out = {}
+    rng = np.random.default_rng(77)
+    meshes = {"chan": _ref_qmesh(RS.channel_grid(3, 2, 2.0, 1.0))}
+    m3, geom = RS.pipe_grid(2, 3, 0.5, 5.0)
+    meshes["pipe"] = RM.promote_to_quadratic(m3, geom)
+    with tempfile.TemporaryDirectory() as td:
+        for name, q in meshes.items():
+            out.update(_mesh_arrays(name, q))
+            vel = rng.normal(size=(q.n_velocity_nodes, q.dim)) * 10.0 ** rng.integers(-8, 8, size=(q.n_velocity_nodes, q.dim))
+            pres = rng.normal(size=q.n_vertices)
+            pres[0] = 0.0
+            if q.n_vertices > 2:
+                pres[1], pres[2] = -0.0, 1e-310          # signed zero, subnormal
+            out[f"{name}_vel"], out[f"{name}_pres"] = vel, pres
+            for fmt in ("native", "vtk"):
+                path = os.path.join(td, f"{name}.{fmt}")
+                RIO.write_field_snapshot(path, q, vel, pres, fmt=fmt, time=0.375)
+                out[f"{name}_{fmt}_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            path = os.path.join(td, f"{name}_geom.vtk")
+            RIO.write_vtk_snapshot(path, q, title="geometry only")
+            out[f"{name}_vtkgeom_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(HERE / "snap.npz", **out)
+    print("snapshots", {k: v.size for k, v in out.items() if k.endswith("_bytes")})
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d", "post"]
+    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d", "post", "snap"]
     with Pool(min(9, os.cpu_count() or 1)) as pool:
         if "shapes" in what:
             make_shapes()
@@ -319,3 +350,5 @@ if __name__ == "__main__":
             make_small3d(pool)
         if "post" in what:
             make_post()
+        if "snap" in what:
+            make_snapshots()
