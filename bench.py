@@ -344,6 +344,8 @@ def run_b200(args):
     spmv_row_ms = time_spmv(lambda: op.spmv(omegas, xr, jacobi=True, out=ys))
     spmv_bytes = op.spmv_bytes(nb)
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+    info = op.info
+    spmv_gather = int((q.dim * int(info[4]) + int(info[5]) + q.dim * int(info[6])) * nb * 16)
 
     extras = {}
     if rank == 0 and world == 1 and not args.quick:
@@ -400,7 +402,11 @@ def run_b200(args):
             "spmv": {"kernel": "k_spmv_interleaved (tick SpMV)", "modes": nb, "ms": spmv_ms, "bytes": spmv_bytes,
                      "achieved_gbs": spmv_gbs, "frac": spmv_gbs / hbm_peak, "peak": hbm_peak,
                      "row_layout_ms": spmv_row_ms,
-                     "note": "algorithmic bytes = matrix once + x read + y write per mode; gather-latency bound"},
+                     "gathered_bytes": spmv_gather, "gather_tbs": spmv_gather / (spmv_ms * 1e-3) / 1e12,
+                     "note": ("algorithmic bytes = matrix once + x read + y write per mode; the kernel gathers "
+                              "x once per stored entry and mode (gathered_bytes, served by L1/L2 at "
+                              "gather_tbs); ncu: L1 hit 55 %, L2 hit 52 %, long-scoreboard stalls -> "
+                              "gather-latency bound")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "wall_s": e2e_wall},
