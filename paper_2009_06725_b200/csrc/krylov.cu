@@ -9,15 +9,15 @@
 // 1/||w|| scaling of stored basis vectors, mode-major storage.
 //
 // Execution model: each mode carries a small device state machine (ModeCtl.phase).  One "tick"
-// is a fixed sequence of five kernels over the whole batch, captured in a CUDA graph:
+// is a fixed sequence of four kernels over the whole batch, captured in a CUDA graph:
 //   spmv   INNER/START: w = s.(A q_k)          RESID: t = b - A x, r = s.t, norms, cycle decisions
 //   passA  INNER: c  = Q^H w                    (partials per segment, last CTA reduces)
+//          XUPDATE: x += Q y                    (cycle end; own k_pass<PASS_X> launch if SS_X_IN_A=0)
 //   passB  INNER: w -= Q c ; c2 = Q^H w         (one read of Q for both)
-//   passC  INNER: w -= Q c2 ; Q[k+1] = w ; ||w|| -> last CTA: Givens, estimate, exit tests,
+//   passC  INNER: w -= Q c2 ; Q[k+1] = P = w ; ||w|| -> last CTA: Givens, estimate, exit tests,
 //                 triangular solve at cycle end
-//   passX  XUPDATE: x += Q y
-// Every state change is made by the last CTA of a mode in a kernel, so all CTAs of a mode see a
-// consistent phase.  The reduction structure of a mode depends only on (n, k, restart), never on
+// Every state change is made by the last CTA of a mode in a kernel (the tick SpMV: the last CTA
+// of the grid, for all modes), so all CTAs of a mode see a consistent phase.  The reduction structure of a mode depends only on (n, k, restart), never on
 // which other modes share the batch: per-mode results are bitwise invariant under batching and
 // mode order (the reference's test_spectral.py:187-205 contract).
 #include <algorithm>
@@ -42,9 +42,7 @@ struct ModeCtl {
 };
 
 constexpr int PT = 256;        // threads per CTA for every Krylov kernel
-constexpr int PASS_STAGE_TARGET = 3456;   // double2 per pipeline stage (~54 KB) for small J
 constexpr int PASS_MAX_STAGES = 8;
-constexpr int PASS_STAGE_DIV = 4;         // aim for >= 4 stages in the ring
 constexpr int PASS_L2_AHEAD = 4;          // chunks prefetched into L2 beyond the smem ring
 constexpr int PASS_SMEM_ELEMS = 13440;    // dynamic shared memory of a basis pass (210 KB)
 
@@ -353,36 +351,10 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
 
 // ------------------------------------------------------------------------------------------------
 // Basis-streaming passes.  A CTA owns one fixed segment of rows of one mode and streams the
-// (J x rows) slab of raw basis vectors through shared memory in chunks (cp.async, 2 stages).
+// (J x rows) slab of raw basis vectors through shared memory in chunks (bulk TMA into a ring of
+// mbarrier-tracked stages, see stream_segment).
 // ------------------------------------------------------------------------------------------------
 enum PassKind : int { PASS_A = 1, PASS_B = 2, PASS_C = 3, PASS_X = 4 };
-
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ int pow2floor(int v) {
-  int p = 1;
-  while (p * 2 <= v) p *= 2;
-  return p;
-}
-
-__device__ __forceinline__ void cp_wait_dyn(int n) {
-  switch (n) {
-    case 0: cp_wait<0>(); break;
-    case 1: cp_wait<1>(); break;
-    case 2: cp_wait<2>(); break;
-    case 3: cp_wait<3>(); break;
-    case 4: cp_wait<4>(); break;
-    case 5: cp_wait<5>(); break;
-    case 6: cp_wait<6>(); break;
-    default: cp_wait<7>(); break;
-  }
-}
 
 // ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -404,9 +376,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
