@@ -139,7 +139,8 @@ def _ref_worker(args):
     for st in range(steps):
         t0 = time.perf_counter()
         costs = [oracle.gmres_inner_step_cost(s.matrix, sc, k, RESTART, np.random.default_rng(k + 7 * st)) for k in STRATA]
-        out.append((float(np.mean(costs)), time.perf_counter() - t0))
+        out.append((float(np.mean(costs)), time.perf_counter() - t0, int(s.matrix.shape[0]), int(s.matrix.nnz),
+                    case.name))
     return out
 
 
@@ -172,8 +173,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, BASELINE config 2)",
-        "config": {"workload": "c2_pipe_199800tets_17modes", "restart": RESTART, "tol": TOL,
-                   "n_dofs": None, "processes": procs},
+        "config": {"workload": res[0][0][4], "modes_per_gpu": 17, "total_modes": 17, "n_dofs": res[0][0][2],
+                   "nnz": res[0][0][3], "restart": RESTART, "iterations_per_mode_per_step": BUDGET, "tol": TOL,
+                   "processes": procs},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": (f"oracle port of krylov.py:63-164 (numpy/scipy, 1 BLAS thread per process), "
                                     f"{procs} processes each timing the exact inner-iteration code path at basis "
