@@ -75,6 +75,7 @@ struct KArgs {
   long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap
   int x_in_a;                  // cycle-end x update inside the next tick's pass-A launch (1) or own launch (0)
   int gthr[3];                 // pass B: largest J using 1, 2, 4 warps per row block (8 above)
+  int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -329,7 +330,20 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   }
   __syncthreads();
   if (s_any_inner) {
-    if (a.kind == 0) {
+    if (a.kind == 0 && a.row_spmv) {
+      // very large n (rule on n only, so per-mode results stay batch-invariant; at most a few modes
+      // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
+      // the mode's column of P with stride pstride (1.7x the interleaved kernel at one mode)
+      for (int b = sub; b < a.nb; b += a.spmv_split) {
+        if (sph[b] != PH_INNER && sph[b] != PH_START) continue;
+        const double om = som[b], xs = sxs[b];
+        double2* w = a.W + (size_t)b * a.ld;
+        saddle_block<DIM>(a.op, sb, om, a.P + b, [&](int row, double2 v) {
+          const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
+          w[row] = cmul(s, cscale(v, xs));
+        }, a.pstride);
+      }
+    } else if (a.kind == 0) {
       spmv_inner_interleaved<DIM>(a, sb, sph, som, sxs);
     } else {
       if (sub == 0)
@@ -1030,6 +1044,14 @@ extern "C" int ss_krylov_create_saddle(const ss_pattern* P, int max_batch, int r
   K->a.kind = 0;
   K->a.op = P->op;
   K->a.nsb = saddle_nsb_host(P->nfree, P->npf);
+  {
+    // row-layout INNER SpMV from 25 M DOFs up (config 5: one mode per GPU at restart 200, where
+    // one lane per row starves the gathers: SpMV -21 %, cycle +5 %; at two modes (config 4) the
+    // interleaved kernel stays ahead).  A rule on n only keeps per-mode results batch-invariant.
+    int64_t thr = 25000000;
+    if (const char* e = getenv("SS_ROW_SPMV_N")) thr = atoll(e);
+    K->a.row_spmv = P->op.n >= thr ? 1 : 0;
+  }
   // sub-CTAs per SpMV row block when there are few blocks: about two (row, mode) pairs of a
   // 128-row block per thread, and no more than needed to fill the GPU (config 1: 9)
   K->a.spmv_split = std::max(1, std::min(std::min(16, (8 * 148 + K->a.nsb - 1) / K->a.nsb),

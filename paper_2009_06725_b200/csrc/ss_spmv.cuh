@@ -86,15 +86,15 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
 // One warp computes pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
 template <int DIM>
 __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int j,
-                                                   const double2* __restrict__ x, int lane) {
+                                                   const double2* __restrict__ x, int lane, int xs = 1) {
   double2 acc = make_double2(0.0, 0.0);
   const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
   for (int e = e0 + lane; e < e1; e += 32) {
-    const double2* xb = x + (size_t)__ldg(op.tcol + e) * DIM;
+    const double2* xb = x + (size_t)__ldg(op.tcol + e) * DIM * xs;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const double dv = __ldg(op.dt + (size_t)e * DIM + d);
-      const double2 v = xb[d];
+      const double2 v = xb[(size_t)d * xs];
       acc.x += dv * v.x;
       acc.y += dv * v.y;
     }
@@ -139,7 +139,8 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
 
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
-                                                  const double2* __restrict__ x, int gl, double2 (&acc)[DIM]) {
+                                                  const double2* __restrict__ x, int gl, double2 (&acc)[DIM],
+                                                  int xs = 1) {
 #pragma unroll
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
   if (r >= 0) {
@@ -149,10 +150,10 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
       const int B = __ldg(op.ncol + e);
       const double2 a = __ldg(op.sm + e);
       const double am = omega * a.y;
-      const double2* xb = x + (size_t)B * DIM;
+      const double2* xb = x + (size_t)B * DIM * xs;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        const double2 v = xb[d];
+        const double2 v = xb[(size_t)d * xs];
         acc[d].x += a.x * v.x - am * v.y;
         acc[d].y += a.x * v.y + am * v.x;
       }
@@ -160,7 +161,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
 #pragma unroll 2
     for (int e = p0 + gl; e < p1; e += 8) {
-      const double2 v = x[op.nfv + __ldg(op.pcol + e)];
+      const double2 v = x[(size_t)(op.nfv + __ldg(op.pcol + e)) * xs];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         const double dv = __ldg(op.dp + (size_t)e * DIM + d);
@@ -178,9 +179,10 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     }
 }
 
+// x is read with stride xs (xs = batch: one mode's column of the mode-interleaved P).
 template <int DIM, class Emit>
 __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, double omega,
-                                             const double2* __restrict__ x, Emit&& emit) {
+                                             const double2* __restrict__ x, Emit&& emit, int xs = 1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nvb = saddle_nvb(op);
   if (blk < nvb) {
@@ -190,7 +192,7 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
       const int r = blk * SPMV_VROWS + it * 32 + warp * 4 + grp;
       const bool ok = r < op.nfree;
       double2 acc[DIM];
-      saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc);
+      saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc, xs);
       if (ok && gl < DIM) {
         double2 v = acc[0];
 #pragma unroll
@@ -204,7 +206,7 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
     for (int it = 0; it < SPMV_PROWS / 8; ++it) {
       const int j = pb * SPMV_PROWS + it * 8 + warp;
       if (j < op.npf) {
-        const double2 v = saddle_pres_row<DIM>(op, j, x, lane);
+        const double2 v = saddle_pres_row<DIM>(op, j, x, lane, xs);
         if (lane == 0) emit(op.nfv + j, v);
       }
     }
