@@ -9,7 +9,7 @@
  *
  * Conventions
  *   - every function returns 0 (SS_OK) or an error code; nothing throws across the ABI;
- *     ss_last_error() returns the message.  Codes: 1 = bad argument (ValueError),
+ *     ss_last_error() returns the calling thread's last message.  Codes: 1 = bad argument (ValueError),
  *     2 = mesh error (MeshError), 3 = CUDA/driver (DeviceError), 4 = misuse (RuntimeError).
  *   - complex128 arrays are interleaved {re, im} doubles;
  *   - pointers named *_dev are device pointers owned by the caller; *_host are host pointers;

@@ -21,21 +21,16 @@
 #include "ss_pattern.h"
 #include "ss_spmv.cuh"
 
-static std::mutex g_err_mu;
-static std::string g_err;
+// Last error message per calling thread (like errno): the pointer ss_last_error returns stays
+// valid until the same thread's next failing call, whatever other threads do.
+static thread_local std::string g_err;
 static int64_t g_launches = 0;
 
-void ss_set_error(const std::string& msg) {
-  std::lock_guard<std::mutex> lk(g_err_mu);
-  g_err = msg;
-}
+void ss_set_error(const std::string& msg) { g_err = msg; }
 void ss_count_launch(int64_t n) { __atomic_fetch_add(&g_launches, n, __ATOMIC_RELAXED); }
 int64_t ss_launch_counter() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
-extern "C" const char* ss_last_error(void) {
-  std::lock_guard<std::mutex> lk(g_err_mu);
-  return g_err.c_str();
-}
+extern "C" const char* ss_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t ss_launch_count(void) { return ss_launch_counter(); }
 extern "C" int ss_version(void) { return 1; }
 
