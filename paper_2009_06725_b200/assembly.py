@@ -358,7 +358,7 @@ class SaddleOperator:
         torch = _lib.torch_mod()
         free, _ = torch.cuda.mem_get_info(self.device)
         per_mode = (restart + 1 + 8) * self.ld * 16 + (restart + 1) * restart * 16
-        return max(1, int(0.85 * free // per_mode))
+        return max(1, min(256, int(0.85 * free // per_mode)))   # 256: krylov.MAX_BATCH
 
 
 _OP_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()

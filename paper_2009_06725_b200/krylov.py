@@ -249,13 +249,31 @@ def gmres_solve(system, settings: SolverSettings, x0=None):
     return x, report
 
 
+MAX_BATCH = 256   # modes per device batch (ss_krylov_create_*: per-tick mode state lives in smem)
+
+
 def gmres_batched(batch, settings: SolverSettings, x0=None, keep_history=True):
-    """Solve every mode of a :class:`~.assembly.ModeSystemBatch` in one device batch.
+    """Solve every mode of a :class:`~.assembly.ModeSystemBatch` in one device batch (chunks of
+    MAX_BATCH modes beyond that; per-mode results do not depend on the chunking).
 
     Returns ``(X, reports)`` with ``X`` the (nb, ld) complex128 device solutions.
     """
     op = batch.operator
     nb = batch.nb
+    if nb > MAX_BATCH:
+        from .assembly import ModeSystemBatch
+
+        torch = _lib.torch_mod()
+        xs, reps = [], []
+        for s in range(0, nb, MAX_BATCH):
+            sl = slice(s, min(nb, s + MAX_BATCH))
+            per_mode = lambda v: None if v is None else v[sl]  # noqa: E731
+            sub = ModeSystemBatch(op, batch.omegas[sl], batch.rhs[sl], per_mode(batch.g), per_mode(batch.dirichlet),
+                                  per_mode(getattr(batch, "loads", None)))
+            X, r = gmres_batched(sub, settings, None if x0 is None else x0[sl], keep_history)
+            xs.append(X)
+            reps.extend(r)
+        return torch.cat(xs, dim=0), reps
     jac = settings.preconditioner == "jacobi"
     ws = op.krylov(settings.restart, nb, max(1, settings.max_iterations))
     wall0, cpu0 = time.perf_counter(), time.thread_time()

@@ -270,3 +270,24 @@ def test_maximum_restart_matches_oracle(c1):
     assert rep.iterations == it == budget
     np.testing.assert_allclose(rep.residual_history, hist, rtol=1e-6)
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+@pytest.mark.gpu
+def test_more_modes_than_one_device_batch(c1):
+    """gmres_batched chunks beyond MAX_BATCH modes; results equal the per-chunk solves bit for bit."""
+    import paper_2009_06725_b200.krylov as K
+
+    case, props, _ = c1
+    settings = SolverSettings(tolerance=1e-6, restart=20, max_iterations=60)
+    h = case.h_modes()
+    idx = [1, 2, 3, 4, 5]
+    full = assemble_mode_systems(case.qmesh, props, case.omegas[idx], None, [h[i] for i in idx])
+    old = K.MAX_BATCH
+    try:
+        K.MAX_BATCH = 2   # force chunking into 2 + 2 + 1
+        Xc, rc = gmres_batched(full, settings)
+    finally:
+        K.MAX_BATCH = old
+    X, r = gmres_batched(full, settings)
+    assert np.array_equal(Xc.cpu().numpy(), X.cpu().numpy())
+    assert [a.iterations for a in rc] == [b.iterations for b in r]
