@@ -40,6 +40,26 @@ def test_library_exports_every_declared_symbol():
     assert set(_lib.SIGNATURES) >= set(_declared_symbols())
 
 
+def _declared_arity():
+    """Parameter count of every ss_* function declared in include/*.h."""
+    out = {}
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        for name, params in re.findall(r"\b(ss_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
+            p = params.strip()
+            out[name] = 0 if p in ("", "void") else p.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_header_arity():
+    """The ctypes table and the C header agree on every entry point's parameter count."""
+    arity = _declared_arity()
+    assert len(arity) >= 40
+    bad = {n: (len(_lib.SIGNATURES[n][1]), a) for n, a in arity.items()
+           if n in _lib.SIGNATURES and len(_lib.SIGNATURES[n][1]) != a}
+    assert not bad, bad
+
+
 def test_library_is_sm100a_code():
     import subprocess
 
