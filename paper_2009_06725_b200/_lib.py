@@ -63,6 +63,7 @@ SIGNATURES = {
     "ss_krylov_create_csr": (I32, [I32, I32, I64, PI32, PI32, I32, PD, PD, I32, I32, I32, I64, C.POINTER(P)]),
     "ss_krylov_destroy": (None, [P]),
     "ss_krylov_info": (I32, [P, PI64]),
+    "ss_krylov_set_option": (I32, [P, C.c_char_p, I64]),
     "ss_krylov_buffers": (I32, [P, C.POINTER(P), C.POINTER(P), PI64]),
     "ss_krylov_solve": (I32, [P, I32, PD, C.POINTER(I32), P, P, I64, I32, D, I64, I32, P, PI64, PD]),
     "ss_krylov_history": (I32, [P, I32, I64, PD]),
@@ -77,6 +78,9 @@ SIGNATURES = {
 
 _lib = None
 
+# Must equal SS_ABI_VERSION in include/spectralstokes_b200.h (bumped whenever an entry point changes).
+ABI_VERSION = 2
+
 
 def load(build_if_missing: bool = True):
     """Load (building in-tree first if needed) the native library."""
@@ -89,6 +93,34 @@ def load(build_if_missing: bool = True):
         from .build import build
         build()
     lib = C.CDLL(str(LIB_PATH))
+    lib.ss_version.restype = I32
+    if lib.ss_version() != ABI_VERSION:
+        # a stale in-tree build (the .so is git-ignored): rebuild once, then refuse
+        if not build_if_missing or os.environ.get("SS_B200_LIB"):
+            raise DeviceError(f"{LIB_PATH} has ABI {lib.ss_version()}, expected {ABI_VERSION}: rebuild it")
+        from .build import build
+        build(force=True)
+        return _load_fresh()
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _load_fresh():
+    """Load a freshly rebuilt library under a new file name (the stale one stays mapped)."""
+    global _lib
+    import shutil
+    import tempfile
+
+    tmp = Path(tempfile.mkdtemp(prefix="ss_b200_")) / LIB_PATH.name
+    shutil.copy2(LIB_PATH, tmp)
+    lib = C.CDLL(str(tmp))
+    lib.ss_version.restype = I32
+    if lib.ss_version() != ABI_VERSION:
+        raise DeviceError(f"rebuilt {LIB_PATH} still reports ABI {lib.ss_version()}, expected {ABI_VERSION}")
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

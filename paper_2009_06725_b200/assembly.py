@@ -15,6 +15,7 @@ materialised lazily as a scipy CSR (bit-identical pattern) only for callers that
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import weakref
 from dataclasses import dataclass
 from pathlib import Path
@@ -208,6 +209,10 @@ class SaddleOperator:
         self._pattern = None
         self._dof = None
         self._krylov = {}
+        # Cached Krylov workspaces hold device RHS/X/basis buffers and a native graph cache: one
+        # host thread at a time per operator (the reference's solve_modes(workers>1) thread pool,
+        # spectral.py:300-305, may call gmres_solve concurrently on systems of one mesh).
+        self.lock = threading.RLock()
 
     @property
     def handle(self):

@@ -40,21 +40,27 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
     nvcc = _nvcc()
-    logs = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = objdir / (src + ".o")
         cmd = [nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if src.endswith(".cpp"):
             cmd.insert(1, "-x")
             cmd.insert(2, "cu")
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, str(obj), subprocess.run(cmd, capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    objs, logs = [], []
+    for src, obj, r in results:
         logs.append(r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
-        objs.append(str(obj))
+        objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fopenmp",
            *objs, "-o", str(tmp), "-lcudart", "-lgomp"]

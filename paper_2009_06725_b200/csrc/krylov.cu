@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <map>
+#include <string>
 #include <vector>
 
 #include "ss_common.h"
@@ -1117,12 +1118,37 @@ extern "C" void ss_krylov_destroy(ss_krylov* K) {
   delete K;
 }
 
+// Workspace options (A/B and parity coverage of layout-dependent code paths).  Changing an option
+// drops the cached graphs.  "row_spmv": 1 = row-layout tick SpMV (8 lanes per node row, strided P
+// column), 0 = mode-interleaved; "device_loop": conditional-WHILE graph; "ticks_per_graph".
+extern "C" int ss_krylov_set_option(ss_krylov* K, const char* name, int64_t value) {
+  if (!K || !name) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  const std::string opt(name);
+  if (opt == "row_spmv") {
+    if (K->a.kind != 0 && value) { ss_set_error("row_spmv applies to the saddle operator only"); return SS_ERR_ARG; }
+    K->a.row_spmv = value ? 1 : 0;
+  } else if (opt == "device_loop") {
+    K->device_loop = value ? 1 : 0;
+  } else if (opt == "ticks_per_graph") {
+    if (value < 1 || value > 1024) { ss_set_error("ticks_per_graph must lie in [1, 1024]"); return SS_ERR_ARG; }
+    K->ticks_per_graph = (int)value;
+  } else {
+    ss_set_error("unknown workspace option '" + opt + "'");
+    return SS_ERR_ARG;
+  }
+  SS_CUDA(cudaSetDevice(K->device));
+  for (auto& kv : K->graphs) cudaGraphExecDestroy(kv.second);
+  K->graphs.clear();
+  return SS_OK;
+}
+
 // info: [n, ld, restart, nseg, seg_rows, nsb, max_batch, ticks_per_graph, smem_pass, kind]
 extern "C" int ss_krylov_info(const ss_krylov* K, int64_t* info) {
   if (!K || !info) { ss_set_error("null argument"); return SS_ERR_ARG; }
   info[0] = K->a.n; info[1] = K->a.ld; info[2] = K->a.restart; info[3] = K->a.nseg; info[4] = K->a.seg_rows;
   info[5] = K->a.nsb; info[6] = K->max_batch; info[7] = K->ticks_per_graph; info[8] = (int64_t)K->smem_pass;
   info[9] = K->a.kind;
+  if (info[10] == -1) { info[10] = K->a.row_spmv; info[11] = K->device_loop; }
   return SS_OK;
 }
 

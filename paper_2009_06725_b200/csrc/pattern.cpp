@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include "spectralstokes_b200.h"
+
 #include "ss_common.h"
 #include "ss_pattern.h"
 #include "ss_spmv.cuh"
@@ -32,7 +34,7 @@ int64_t ss_launch_counter() { return __atomic_load_n(&g_launches, __ATOMIC_RELAX
 
 extern "C" const char* ss_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t ss_launch_count(void) { return ss_launch_counter(); }
-extern "C" int ss_version(void) { return 1; }
+extern "C" int ss_version(void) { return SS_ABI_VERSION; }
 
 template <class T>
 static int upload(ss_pattern* P, const std::vector<T>& h, T** d) {

@@ -77,6 +77,16 @@ class KrylovWorkspace:
     def close(self):
         self._finalizer()
 
+    def set_option(self, name: str, value: int):
+        """Native workspace option (``ss_krylov_set_option``): "row_spmv", "device_loop", "ticks_per_graph"."""
+        _lib.call("ss_krylov_set_option", self._h, name.encode(), int(value))
+
+    def options(self):
+        info = np.zeros(12, dtype=np.int64)
+        info[10] = -1
+        _lib.call("ss_krylov_info", self._h, _lib.ptr(info, C.c_int64))
+        return {"row_spmv": int(info[10]), "device_loop": int(info[11]), "ticks_per_graph": int(info[7])}
+
     @classmethod
     def for_operator(cls, op, restart: int, max_batch: int, hist_cap: int):
         if restart > MAX_RESTART:
@@ -217,6 +227,8 @@ def gmres_solve(system, settings: SolverSettings, x0=None):
 
     jac = settings.preconditioner == "jacobi"
     wall0, cpu0 = time.perf_counter(), time.thread_time()
+    if not isinstance(system, (tuple, ComplexSaddleSystem)) and hasattr(system, "matrix") and hasattr(system, "rhs"):
+        system = (system.matrix, system.rhs)   # a system assembled by other code (e.g. the reference's CPU path)
     if isinstance(system, tuple):
         matrix, rhs = system
         n = matrix.shape[0]
@@ -234,13 +246,15 @@ def gmres_solve(system, settings: SolverSettings, x0=None):
             ws.close()
     elif isinstance(system, ComplexSaddleSystem):
         op = system.operator
-        ws = op.krylov(settings.restart, 1, max(1, settings.max_iterations))
-        x0d = None if x0 is None else _to_device_rows(x0, ws.ld, ws.device)
-        out = ws.solve([system.omega], system._rhs_dev, x0d, settings.tolerance, settings.max_iterations, jacobi=jac)
-        wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
-        res = float(ws.residuals(1)[0])
-        x = out["x"][0, : op.n].cpu().numpy()
-        hist = ws.history(0, int(out["hist_len"][0]))
+        with op.lock:
+            ws = op.krylov(settings.restart, 1, max(1, settings.max_iterations))
+            x0d = None if x0 is None else _to_device_rows(x0, ws.ld, ws.device)
+            out = ws.solve([system.omega], system._rhs_dev, x0d, settings.tolerance, settings.max_iterations,
+                           jacobi=jac)
+            wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
+            res = float(ws.residuals(1)[0])
+            x = out["x"][0, : op.n].cpu().numpy()
+            hist = ws.history(0, int(out["hist_len"][0]))
     else:
         raise TypeError("system must be a ComplexSaddleSystem or a (matrix, rhs) tuple")
     report = SolveReport(iterations=int(out["iterations"][0]), residual=res,
@@ -275,14 +289,16 @@ def gmres_batched(batch, settings: SolverSettings, x0=None, keep_history=True):
             reps.extend(r)
         return torch.cat(xs, dim=0), reps
     jac = settings.preconditioner == "jacobi"
-    ws = op.krylov(settings.restart, nb, max(1, settings.max_iterations))
-    wall0, cpu0 = time.perf_counter(), time.thread_time()
-    out = ws.solve(batch.omegas, batch.rhs, x0, settings.tolerance, settings.max_iterations, jacobi=jac)
-    wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
-    res = ws.residuals(nb)
+    with op.lock:
+        ws = op.krylov(settings.restart, nb, max(1, settings.max_iterations))
+        wall0, cpu0 = time.perf_counter(), time.thread_time()
+        out = ws.solve(batch.omegas, batch.rhs, x0, settings.tolerance, settings.max_iterations, jacobi=jac)
+        wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
+        res = ws.residuals(nb)
+        hists = [ws.history(b, int(out["hist_len"][b])) if keep_history else [] for b in range(nb)]
     reports = []
     for b in range(nb):
-        hist = ws.history(b, int(out["hist_len"][b])) if keep_history else []
+        hist = hists[b]
         reports.append(SolveReport(iterations=int(out["iterations"][b]), residual=float(res[b]),
                                    converged=bool(out["converged"][b] and res[b] <= settings.tolerance),
                                    wall_time=wall, cpu_time=cpu, residual_history=hist))

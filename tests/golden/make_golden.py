@@ -21,6 +21,11 @@ Fixtures
                   pipe), two modes each solved by the reference to 1e-10
   snap.npz        field snapshots written by the reference (native text + legacy VTK, 2D and 3D)
                   as raw bytes, with their inputs                              (io.py:88-183)
+  c2_gmres.npz    BASELINE config 2 fixed-budget GMRES (modes 1, 16; restart 200, 200 iterations,
+                  x0 = 0): residual history, x at sampled rows, ||x|| and projections of x on
+                  seeded vectors                                                 (krylov.py:63-164)
+  adaptive.npz    adaptive_mode_refinement on seeded sampled waveforms: final N_m, converged flag,
+                  per-mode energies and iteration counts                       (spectral.py:333-371)
   post.npz        post-processing on seeded complex fields: interpolate_at_quadrature, l2_norm,
                   field_error vs an analytic point oracle, flow_rate and patch_area of every
                   boundary patch, fit_loglog_slope             (assembly.py:497-511, metrics.py:12-113)
@@ -264,6 +269,76 @@ def make_c2_pattern():
     print("c2 pattern", time.perf_counter() - t0, "s")
 
 
+# -- config 2 fixed-budget GMRES (x and history after 200 iterations) ---------------
+
+C2_GMRES_MODES = (1, 16)
+C2_GMRES_SAMPLE = 20000
+
+
+def _c2_gmres(idx):
+    case = c2_case()
+    q = _ref_qmesh(case.mesh, "cylinder", case.radius)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    s = RA.assemble_mode_system(q, props, float(case.omegas[idx]), g_mode=case.coefficients[idx] * case.profile)
+    sc = RK.jacobi_precondition(s)
+    t0 = time.perf_counter()
+    x, it, hist, conv = RK.gmres(s.matrix, s.rhs, tol=1e-10, restart=200, maxiter=200, scale=sc)
+    wall = time.perf_counter() - t0
+    n = s.n_dofs
+    rows = np.sort(np.random.default_rng(1000 + idx).choice(n, C2_GMRES_SAMPLE, replace=False))
+    rng = np.random.default_rng(2000 + idx)
+    proj = np.stack([rng.normal(size=n) + 1j * rng.normal(size=n) for _ in range(4)]) @ x
+    return idx, dict(hist=np.array(hist), iters=np.int64(it), conv=np.bool_(conv), rows=rows, x_rows=x[rows],
+                     x_norm=np.float64(np.linalg.norm(x)), proj=proj, n=np.int64(n), wall=np.float64(wall),
+                     res=np.float64(np.linalg.norm(s.rhs - s.matrix @ x) / np.linalg.norm(s.rhs)))
+
+
+def make_c2_gmres(pool):
+    out = {}
+    for idx, d in pool.map(_c2_gmres, C2_GMRES_MODES):
+        for k, v in d.items():
+            out[f"{k}_{idx}"] = v
+        print("c2 gmres mode", idx, "iters", int(d["iters"]), "wall", float(d["wall"]), "res", float(d["res"]))
+    np.savez_compressed(HERE / "c2_gmres.npz", **out)
+
+
+# -- adaptive mode refinement (spectral.py:333-371) -------------------------------------------------
+
+ADAPTIVE_CASES = {
+    # name: (signal, period, kind, tol, max_modes)
+    "square": ("square", 10.0, "neumann", 1e-3, 12),
+    "square_tight": ("square", 10.0, "neumann", 1e-6, 9),
+    "noisy": ("noisy", 1.0, "neumann", 2e-2, 16),
+}
+
+
+def adaptive_signal(kind, n=128):
+    """Seeded sampled signals for the adaptive fixture (shared with tests/test_gpu_postprocess.py)."""
+    t = np.arange(n) / n
+    if kind == "square":
+        return np.where(t < 0.5, 1.0, -1.0)
+    rng = np.random.default_rng(333)
+    return np.sin(2 * np.pi * t) + 0.3 * np.sin(6 * np.pi * t + 0.4) + 0.05 * rng.normal(size=n)
+
+
+def make_adaptive():
+    out = {}
+    q = RM.promote_to_quadratic(RS.channel_grid(6, 3, length=2.0, half_height=1.0))
+    props = RA.FluidProps(density=1.0, viscosity=1.0)
+    for name, (sig, period, kind, tol, mm) in ADAPTIVE_CASES.items():
+        wf = RSP.BoundaryWaveform(patch="inlet", kind=kind, direction=np.array([1.0, 0.0]), period=period,
+                                  samples=adaptive_signal(sig))
+        sols, final_nm, conv = RSP.adaptive_mode_refinement(q, props, [wf], tol,
+                                                            RK.SolverSettings(tolerance=1e-10), max_modes=mm)
+        out[f"{name}_final_nm"], out[f"{name}_converged"] = np.int64(final_nm), np.bool_(conv)
+        out[f"{name}_n_solved"] = np.int64(len(sols))
+        out[f"{name}_energies"] = RSP.mode_energies(sols, q, period)
+        out[f"{name}_iters"] = np.array([s.report.iterations for s in sols])
+        out[f"{name}_u_last"] = sols[-1].velocity
+        print("adaptive", name, final_nm, conv, len(sols))
+    np.savez_compressed(HERE / "adaptive.npz", **out)
+
+
 def post_oracle(xy):
     """Analytic point field for field_error (shared with tests/test_*_post.py): complex, dim-vector."""
     x = np.asarray(xy, dtype=float)
@@ -334,7 +409,8 @@ def make_snapshots():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d", "post", "snap"]
+    what = sys.argv[1:] or ["shapes", "meshes", "c2", "c1", "pipe3d", "small3d", "post", "snap", "c2gmres",
+                            "adaptive"]
     with Pool(min(9, os.cpu_count() or 1)) as pool:
         if "shapes" in what:
             make_shapes()
@@ -352,3 +428,7 @@ if __name__ == "__main__":
             make_post()
         if "snap" in what:
             make_snapshots()
+        if "c2gmres" in what:
+            make_c2_gmres(pool)
+        if "adaptive" in what:
+            make_adaptive()

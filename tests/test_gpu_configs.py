@@ -5,8 +5,7 @@
 * Full-size meshes (2.06 M / 4.96 M / 8.0 M tets) are checked where the CPU cannot go: pattern rows
   bit-exact, A@x and rhs at sampled rows against the oracle's exact sampled-row assembly
   (`oracle.sampled_rows`), and the GMRES contracts (monotone estimates within a cycle, reported
-  true residual = independent re-measure) on a fixed iteration budget.  Config 3 runs by default;
-  configs 4 and 5 need SS_FULL_CONFIGS=1 (minutes of host mesh generation).
+  true residual = independent re-measure) on a fixed iteration budget, for all three configs.
 """
 
 import hashlib
@@ -106,14 +105,12 @@ def test_config3_full_size():
     _full_size_checks(case, [1, 63])
 
 
-@pytest.mark.skipif(os.environ.get("SS_FULL_CONFIGS") != "1", reason="set SS_FULL_CONFIGS=1 (minutes of mesh build)")
 def test_config4_full_size():
     case = c4_case()
     assert case.mesh.n_elements > 4_900_000
     _full_size_checks(case, [1, 31])
 
 
-@pytest.mark.skipif(os.environ.get("SS_FULL_CONFIGS") != "1", reason="set SS_FULL_CONFIGS=1 (minutes of mesh build)")
 def test_config5_full_size():
     case = c5_case()
     assert case.mesh.n_elements > 7_900_000
