@@ -46,6 +46,7 @@ constexpr int PT = 256;        // threads per CTA for every Krylov kernel
 constexpr int PASS_MAX_STAGES = 8;
 constexpr int PASS_L2_AHEAD = 4;          // chunks prefetched into L2 beyond the smem ring
 constexpr int PASS_SMEM_ELEMS = 13440;    // dynamic shared memory of a basis pass (210 KB)
+constexpr int WIDE_RESTART = 240;         // largest restart served by the TMA-ring passes (J <= 241)
 
 struct KArgs {
   int kind;                    // 0 saddle, 1 csr
@@ -77,6 +78,7 @@ struct KArgs {
   int x_in_a;                  // cycle-end x update inside the next tick's pass-A launch (1) or own launch (0)
   int gthr[3];                 // pass B: largest J using 1, 2, 4 warps per row block (8 above)
   int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
+  int wide;                    // restart > WIDE_RESTART: basis passes without the shared-memory ring (any J)
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -555,6 +557,93 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   }
 }
 
+// Basis pass for restart > WIDE_RESTART (any J): the same two phases as stream_segment, reading the
+// basis straight from global memory (lanes = rows of a 32-row block, coalesced 512-B rows; warps
+// split the columns) instead of through the shared-memory ring, whose stage must hold a whole
+// J x 32 block.  Dots are taken in tiles of 256 columns (32 register accumulators per thread).
+// Coefficients come from global memory: B/C: qs_j * C{1,2}_j, X: Y_j.
+template <int PASS>
+__device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s, int J, int k, double2* red,
+                                                    double2* part) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int segb = a.seg_rows / RB;
+  const int blk_begin = s * segb;
+  const int blk_end = min(blk_begin + segb, a.nblk);
+  double2* vec = (PASS == PASS_X ? a.X : a.W) + (size_t)b * a.ld;
+  const double* qs = a.qs + (size_t)b * a.jcap;
+  const double2* cc = (PASS == PASS_B ? a.C1 : PASS == PASS_C ? a.C2 : a.Y) + (size_t)b * a.jcap;
+  double nrm = 0.0;
+  if (PASS != PASS_A) {
+    for (int blk = blk_begin; blk < blk_end; ++blk) {
+      const double2* S = qblock(a, b, blk) + lane;
+      double2 p = make_double2(0.0, 0.0);
+#pragma unroll 4
+      for (int j = warp; j < J; j += PT / 32) {
+        const double2 q = S[(size_t)j * RB];
+        const double2 cf = PASS == PASS_X ? cc[j] : cscale(cc[j], qs[j]);
+        p.x += q.x * cf.x - q.y * cf.y;
+        p.y += q.x * cf.y + q.y * cf.x;
+      }
+      red[tid] = p;
+      __syncthreads();
+      if (warp == 0) {
+        double2 tot = red[lane];
+#pragma unroll
+        for (int w = 1; w < PT / 32; ++w) tot = cadd(tot, red[w * 32 + lane]);
+        const int64_t row = (int64_t)blk * RB + lane;
+        const double2 v = PASS == PASS_X ? cadd(vec[row], tot) : csub(vec[row], tot);
+        if (PASS == PASS_C) {
+          qblock(a, b, blk)[(size_t)(k + 1) * RB + lane] = v;   // raw q_{k+1}
+          a.P[(size_t)row * a.pstride + b] = v;
+          nrm += cabs2(v);
+        } else {
+          vec[row] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (PASS == PASS_A || PASS == PASS_B) {
+    for (int j0 = 0; j0 < J; j0 += PT) {
+      double2 acc[PT / 8];
+#pragma unroll
+      for (int t = 0; t < PT / 8; ++t) acc[t] = make_double2(0.0, 0.0);
+      for (int blk = blk_begin; blk < blk_end; ++blk) {
+        const double2 v = vec[(int64_t)blk * RB + lane];
+        const double2* S = qblock(a, b, blk) + lane;
+#pragma unroll
+        for (int t = 0; t < PT / 8; ++t) {
+          const int j = j0 + warp + 8 * t;
+          if (j < J) {
+            const double2 q = S[(size_t)j * RB];
+            acc[t].x += q.x * v.x + q.y * v.y;
+            acc[t].y += q.x * v.y - q.y * v.x;
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < PT / 8; ++t) {
+        const int j = j0 + warp + 8 * t;
+        const double x = warp_sum(acc[t].x), y = warp_sum(acc[t].y);
+        if (lane == 0 && j < J) part[j] = make_double2(x, y);
+      }
+    }
+  }
+  if (tid == 0 && blk_begin * RB < a.n) {
+    const int64_t real_rows = min((int64_t)blk_end * RB, (int64_t)a.n) - (int64_t)blk_begin * RB;
+    atomicAdd(a.bytes + PASS, (unsigned long long)((J + (PASS == PASS_A ? 1 : 2)) * real_rows * 16));
+  }
+  if (PASS == PASS_C) {
+    red[tid] = make_double2(nrm, 0.0);
+    __syncthreads();
+    for (int o = PT / 2; o > 0; o >>= 1) {
+      if (tid < o) red[tid].x += red[tid + o].x;
+      __syncthreads();
+    }
+    if (tid == 0) part[0] = red[0];
+  }
+}
+
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -690,9 +779,13 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   if (PASS == PASS_A && phase == PH_XUPDATE && a.x_in_a) {
     // cycle-end x += Q y rides on the next tick's pass-A launch (one launch per tick saved)
     const int kx = c->k;
-    for (int j = tid; j < kx; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
-    __syncthreads();
-    stream_segment<PASS_X, 1>(a, b, s, kx, kx, coef, smem, mbar, red, nullptr);
+    if (a.wide) {
+      stream_segment_wide<PASS_X>(a, b, s, kx, kx, red, nullptr);
+    } else {
+      for (int j = tid; j < kx; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
+      __syncthreads();
+      stream_segment<PASS_X, 1>(a, b, s, kx, kx, coef, smem, mbar, red, nullptr);
+    }
     if (!last_cta(a, b, PASS_X, a.nseg, &sflag)) return;
     if (tid == 0) c->phase = PH_RESID;
     return;
@@ -701,6 +794,11 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   const int k = c->k;
   const int J = PASS == PASS_X ? k : k + 1;
   double* qs = a.qs + (size_t)b * a.jcap;
+  double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
+  const int T = (J + 7) / 8;
+  if (a.wide) {
+    stream_segment_wide<PASS>(a, b, s, J, k, red, part);
+  } else {
   // coefficients of the update (qs folded in): B: qs_j c_j, C: qs_j c2_j, X: y_j (already scaled)
   if (PASS == PASS_B || PASS == PASS_C) {
     const double2* cc = (PASS == PASS_B ? a.C1 : a.C2) + (size_t)b * a.jcap;
@@ -709,8 +807,6 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     for (int j = tid; j < J; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
   }
   __syncthreads();
-  double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
-  const int T = (J + 7) / 8;
   if (PASS == PASS_B && J <= a.gthr[2]) {
     if (J <= a.gthr[0]) {
       if (J <= 4) stream_segment_bg<1, 4>(a, b, s, J, coef, smem, mbar, red, part);
@@ -731,6 +827,7 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   } else {
     stream_segment<PASS, 1>(a, b, s, J, k, coef, smem, mbar, red, part);
   }
+  }   // !a.wide
   if (PASS == PASS_X) {
     if (!last_cta(a, b, PASS, a.nseg, &sflag)) return;
     if (tid == 0) c->phase = PH_RESID;
@@ -740,11 +837,14 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
 
   // ---- last CTA of this mode: reduce partials over segments in fixed order ----
   const double2* pb = a.part + (size_t)b * a.nseg * a.jcap;
-  const int JR = PASS == PASS_C ? 1 : J;
-  const int SL = max(1, PT / JR);      // slices over segments
+  const int JA = PASS == PASS_C ? 1 : J;
+  int SL = 1;
+  for (int jb = 0; jb < JA; jb += PT) {   // one tile unless J > 256 (wide restart)
+  const int JR = min(PT, JA - jb);
+  SL = max(1, PT / JR);      // slices over segments
   {
     // 8 independent accumulators keep 8 L2 loads in flight per thread; combined in fixed order
-    const int j = tid % JR, sl = tid / JR;
+    const int j = jb + tid % JR, sl = tid / JR;
     double2 acc8[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc8[u] = make_double2(0.0, 0.0);
@@ -770,18 +870,23 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     if (tid < JR) {
       double2 acc = red[tid];
       for (int q = 1; q < SL; ++q) acc = cadd(acc, red[q * JR + tid]);
-      out[tid] = cscale(acc, qs[tid]);
+      out[jb + tid] = cscale(acc, qs[jb + tid]);
     }
-    return;
+    __syncthreads();
   }
+  }
+  if (PASS == PASS_A || PASS == PASS_B) return;
   // PASS_C: Givens update (krylov.py:115-149).  The H column and the stored rotations are staged
   // in (now idle) shared memory by all threads; one thread runs the serial recurrence on them.
-  __shared__ double2 y[256];
+  __shared__ double2 ys[256];
   __shared__ int s_solve;
   const int jc = a.jcap;
-  double2* hs = smem;               // column k (k+2 entries)
-  double2* css = smem + 256;        // cs[0..k)
-  double2* sns = smem + 512;        // sn[0..k)
+  // wide restart: the column, rotations and y live in global memory (H column k, CS, SN, Y)
+  double2* hcol = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
+  double2* hs = a.wide ? hcol : smem;                           // column k (k+2 entries)
+  const double2* css = a.wide ? a.CS + (size_t)b * a.restart : smem + 256;   // cs[0..k)
+  const double2* sns = a.wide ? a.SN + (size_t)b * a.restart : smem + 512;   // sn[0..k)
+  double2* y = a.wide ? a.Y + (size_t)b * jc : ys;
   {
     const double2* c1 = a.C1 + (size_t)b * jc;
     const double2* c2 = a.C2 + (size_t)b * jc;
@@ -789,7 +894,7 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     const double2* sng = a.SN + (size_t)b * a.restart;
     for (int i = tid; i <= k; i += PT) {
       hs[i] = cadd(c1[i], c2[i]);
-      if (i < k) { css[i] = csg[i]; sns[i] = sng[i]; }
+      if (i < k && !a.wide) { smem[256 + i] = csg[i]; smem[512 + i] = sng[i]; }
     }
   }
   __syncthreads();
@@ -853,10 +958,8 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     }
   }
   __syncthreads();
-  {
-    double2* hg = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
-    for (int i = tid; i <= k + 1; i += PT) hg[i] = hs[i];
-  }
+  if (!a.wide)
+    for (int i = tid; i <= k + 1; i += PT) hcol[i] = hs[i];
   __syncthreads();
   const int kk = s_solve;
   if (kk == 0) return;
@@ -872,7 +975,7 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
     for (int i = tid; i < j; i += PT) y[i] = csub(y[i], cmul(hb[(size_t)j * jc + i], yj));
     __syncthreads();
   }
-  for (int i = tid; i < kk; i += PT) a.Y[(size_t)b * jc + i] = cscale(y[i], qs[i]);
+  for (int i = tid; i < kk; i += PT) a.Y[(size_t)b * jc + i] = cscale(y[i], qs[i]);   // in place when wide
   __syncthreads();
   if (tid == 0) c->phase = PH_XUPDATE;
 }
@@ -953,7 +1056,7 @@ static int kalloc(ss_krylov* K, size_t count, T** p) {
 }
 
 static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, int64_t hist_cap) {
-  if (restart < 1 || restart > 240) { ss_set_error("restart must lie in [1, 240]"); return SS_ERR_ARG; }
+  if (restart < 1 || restart > (1 << 20)) { ss_set_error("restart must lie in [1, 2^20]"); return SS_ERR_ARG; }
   if (max_batch < 1 || max_batch > MAXB_SMEM) { ss_set_error("max_batch must lie in [1, 256]"); return SS_ERR_ARG; }
   KArgs& a = K->a;
   a.n = n;
@@ -976,7 +1079,9 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   a.smem_elems = PASS_SMEM_ELEMS;
   a.stage_div = 0;   // 0 = per-pass default
   if (const char* e = getenv("SS_PASS_SMEM")) a.smem_elems = std::max(2048, std::min(PASS_SMEM_ELEMS, atoi(e)));
-  a.smem_elems = std::max(a.smem_elems, a.jcap * RB + 2 * RB);   // one full-J block + vector must fit a stage
+  a.wide = restart > WIDE_RESTART ? 1 : 0;
+  if (!a.wide) a.smem_elems = std::max(a.smem_elems, a.jcap * RB + 2 * RB);   // one full-J block + vector must fit a stage
+  else a.smem_elems = 3 * 256;                                                  // no ring; pass C staging unused
   if (const char* e = getenv("SS_PASS_DIV")) a.stage_div = std::max(1, atoi(e));
   K->max_batch = max_batch;
   const size_t B = max_batch;

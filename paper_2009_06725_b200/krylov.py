@@ -21,6 +21,8 @@ from . import _lib
 __all__ = ["SolverSettings", "SolveReport", "jacobi_precondition", "gmres", "gmres_solve", "gmres_batched",
            "KrylovWorkspace", "MAX_RESTART"]
 
+# Largest restart served by the shared-memory-ring basis passes; larger restarts (any value >= 1, as
+# the reference accepts, krylov.py:24,31-32) run the wide passes that read the basis from global memory.
 MAX_RESTART = 240
 
 
@@ -89,8 +91,6 @@ class KrylovWorkspace:
 
     @classmethod
     def for_operator(cls, op, restart: int, max_batch: int, hist_cap: int):
-        if restart > MAX_RESTART:
-            raise ValueError(f"restart > {MAX_RESTART} is not supported by the device GMRES engine")
         h = C.c_void_p()
         _lib.call("ss_krylov_create_saddle", op.handle, int(max_batch), int(restart), int(hist_cap), C.byref(h))
         return cls(h, op.device, restart, max_batch, hist_cap, op.n, keep=op)
@@ -101,8 +101,6 @@ class KrylovWorkspace:
         import scipy.sparse as sp
 
         torch = _lib.torch_mod()
-        if restart > MAX_RESTART:
-            raise ValueError(f"restart > {MAX_RESTART} is not supported by the device GMRES engine")
         dev = torch.cuda.current_device() if device is None else int(device)
         a = sp.csr_matrix(matrix, dtype=complex)
         n = a.shape[0]

@@ -305,20 +305,23 @@ def make_c2_gmres(pool):
 # -- adaptive mode refinement (spectral.py:333-371) -------------------------------------------------
 
 ADAPTIVE_CASES = {
-    # name: (signal, period, kind, tol, max_modes)
-    "square": ("square", 10.0, "neumann", 1e-3, 12),
-    "square_tight": ("square", 10.0, "neumann", 1e-6, 9),
-    "noisy": ("noisy", 1.0, "neumann", 2e-2, 16),
+    # name: (signal, period, kind, tol, max_modes)   -> reference outcome (final N_m, converged, solved)
+    "square": ("square", 10.0, "neumann", 1e-3, 12),    # stops at the zero even harmonic: (1, True, 3)
+    "saw": ("saw", 1.0, "neumann", 1e-2, 20),            # (11, True, 12)
+    "saw_cap": ("saw", 1.0, "neumann", 2e-3, 16),        # hits max_modes: (16, False, 17)
+    "noisy": ("noisy", 10.0, "neumann", 1e-2, 16),       # (8, True, 9)
 }
 
 
 def adaptive_signal(kind, n=128):
-    """Seeded sampled signals for the adaptive fixture (shared with tests/test_gpu_postprocess.py)."""
+    """Seeded sampled signals for the adaptive fixture (tests/test_gpu_postprocess.py rebuilds them)."""
     t = np.arange(n) / n
     if kind == "square":
         return np.where(t < 0.5, 1.0, -1.0)
+    if kind == "saw":
+        return t - 0.5
     rng = np.random.default_rng(333)
-    return np.sin(2 * np.pi * t) + 0.3 * np.sin(6 * np.pi * t + 0.4) + 0.05 * rng.normal(size=n)
+    return np.sin(2 * np.pi * t) + 0.3 * np.sin(6 * np.pi * t + 0.4) + 0.2 * rng.normal(size=n)
 
 
 def make_adaptive():

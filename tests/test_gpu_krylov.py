@@ -291,3 +291,56 @@ def test_more_modes_than_one_device_batch(c1):
     X, r = gmres_batched(full, settings)
     assert np.array_equal(Xc.cpu().numpy(), X.cpu().numpy())
     assert [a.iterations for a in rc] == [b.iterations for b in r]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("restart", [241, 300])
+def test_wide_restart_matches_oracle(c1, restart):
+    """restart > 240 (the reference accepts any restart >= 1, krylov.py:24,31-32): the wide basis
+    passes (no shared-memory ring, dots in 256-column tiles, Givens/solve staging in global memory)
+    against the oracle's CGS2 GMRES over one full cycle plus a few iterations of the next."""
+    from oracle import scvs
+
+    case, props, _ = c1
+    s = assemble_mode_system(case.qmesh, props, case.omegas[3], h_mode=case.h_modes()[3])
+    budget = restart + 7
+    x, rep = gmres_solve(s, SolverSettings(tolerance=C1_TOL, restart=restart, max_iterations=budget))
+    a = s.matrix
+    xo, it, hist, _ = scvs.gmres(a, s.rhs, C1_TOL, restart, budget, scvs.jacobi_scale(a))
+    assert rep.iterations == it == budget
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=1e-6)
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+@pytest.mark.gpu
+def test_wide_restart_converges_generic_csr():
+    """gmres(matrix, ...) with restart 600 on a generic complex CSR: converged like the oracle."""
+    from oracle import scvs
+
+    rng = np.random.default_rng(21)
+    n = 700
+    a = sp.random(n, n, density=0.01, random_state=np.random.RandomState(4), dtype=float)
+    a = (a + 1j * sp.random(n, n, density=0.01, random_state=np.random.RandomState(5))).tocsr()
+    a = a + sp.diags(3.0 + rng.random(n))
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    sc = scvs.jacobi_scale(a)
+    x, it, hist, conv = gmres(a, b, tol=1e-11, restart=600, maxiter=2000, scale=sc)
+    xo, ito, histo, convo = scvs.gmres(a, b, 1e-11, 600, 2000, sc)
+    assert conv and convo and it == ito
+    np.testing.assert_allclose(hist, histo, rtol=1e-6)
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+@pytest.mark.gpu
+def test_wide_restart_through_solve_modes():
+    """solve_modes with SolverSettings(restart=320) converges to the reference's fields (c1 mode 4)."""
+    from paper_2009_06725_b200 import solve_mode_systems
+
+    case = c1_case()
+    props = FluidProps(case.density, case.viscosity)
+    g = golden("c1.npz")
+    sols = solve_mode_systems(case.qmesh, props, [4], case.omegas[[4]], None, [case.h_modes()[4]],
+                              SolverSettings(tolerance=C1_TOL, restart=320))
+    s = sols[0]
+    assert s.report.converged
+    assert np.linalg.norm(s.velocity - g["u_4"]) <= 1e-7 * np.linalg.norm(g["u_4"])
