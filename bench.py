@@ -1,25 +1,29 @@
-"""Benchmark: BASELINE config 2 (3D pipe, 199 800 jittered tets, 17 Fourier modes, complex128).
+"""Benchmark: BASELINE config 5 -- the mode-scaling sweep on the 8 M-tet jittered pipe, 128 modes.
 
-A step is one pass of the hot path over the config's mode batch: one full restarted-GMRES cycle
-(restart 200, i.e. 200 inner iterations per mode: SpMV + CGS2 + Givens, then the cycle-end
-solve, x update and true residual) for every mode, from x0 = 0 on the assembled right-hand
-sides.  Config 2 cannot be converged at 1e-10 inside a benchmark (~10^5+
-iterations per mode), so the rate is reported as GMRES mode-iterations per second at that fixed
-budget, with the projected modes/s labelled as a projection; config 1 (2D channel, which does
-converge) is also solved to 1e-10 and reported as measured modes/s.
+Workload (BASELINE.json configs[4], the largest config that fits one GPU): 8 004 150 tets,
+n = 32 937 682 reduced DOFs, nnz = 1 405 049 508, rho = 1.06, mu = 0.04, parabolic Dirichlet inlet
+x Q_n with q_n ~ (N + iN)/(1 + n^2) (seed 5), modes 0..127, complex128.  At restart 200 one mode's
+Krylov basis is 106 GB, so one mode at a time runs per GPU.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+A step is one pass of the hot path for one mode on every GPU: the mode's right-hand side is
+assembled on the device and one full restarted-GMRES cycle runs (restart 200: 200 inner iterations
+of SpMV + CGS2 + Givens, then the triangular solve, x update and true residual), from x0 = 0.
+Rank r walks its LPT shard of the 128 modes (plan by expected iterations); config 5 cannot be
+converged at 1e-10 inside a benchmark, so the rate is GMRES mode-iterations per
+second.  Measured 3D modes solved/s come from the down-scaled pipes solved to 1e-10 in the same run
+(`c3d_converged`) and the 2D config 1 (`c1_converged`).
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling, each rank owns a 17-mode batch of a
-17*N-mode set (modes are independent; LPT shard, no data-path collective; the solved modal
-fields are all-gathered once per step over NCCL).
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c5|c2]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- every rank runs one mode-cycle per step
+from its shard, no data-path collective; in the end-to-end leg the solved modal fields of every
+step are gathered to rank 0 with the library's NCCL communicator (ss_comm_gather_modes).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -39,6 +43,26 @@ UNIT = "GMRES mode-iterations/s"
 RESTART = 200
 BUDGET = 200           # inner iterations per mode per step (one restart cycle)
 TOL = 1e-10
+STRATA = (0, 50, 100, 150, 199)
+
+# The workloads' identity (checked against the built operator in the B200 arm, so both arms print
+# the same config dict).
+WORKLOADS = {
+    "c5": dict(workload="c5_pipe_8004150tets", n_dofs=32937682, nnz=1405049508, total_modes=128,
+               modes_per_gpu_per_step=1, slab_layers=9),
+    "c2": dict(workload="c2_pipe_199800tets", n_dofs=796978, nnz=32911596, total_modes=17,
+               modes_per_gpu_per_step=17, slab_layers=None),
+}
+
+
+def config_dict(key):
+    w = WORKLOADS[key]
+    return {"workload": w["workload"], "total_modes": w["total_modes"],
+            "modes_per_gpu_per_step": w["modes_per_gpu_per_step"], "n_dofs": w["n_dofs"], "nnz": w["nnz"],
+            "restart": RESTART, "iterations_per_mode_per_step": BUDGET, "tol": TOL, "x0": "zero",
+            "mode_plan": "LPT over expected iterations (distributed.expected_iterations, 3D model); "
+                         "rank r runs plan[r][step % len(plan[r])]",
+            "l2": "inputs larger than L2 (Krylov basis 201 x n x 16 B per mode >> 126 MB)"}
 
 
 def peaks():
@@ -105,47 +129,71 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-# CPU baselines (oracle port of the reference; test infrastructure, never the product path)
+# CPU legs: the oracle port of the reference (test infrastructure, never the product path)
 # ------------------------------------------------------------------------------------------------
 
-STRATA = (0, 50, 100, 150, 199)
+def _oracle_case(key):
+    from paper_2009_06725_b200.workloads import c2_case, c5_slab
+
+    return c5_slab(WORKLOADS[key]["slab_layers"]) if key == "c5" else c2_case()
 
 
-def _oracle_cycle_cost(seed_mode: int = 1):
-    """Seconds per inner GMRES iteration of the oracle port on config 2, averaged over a restart
-    cycle by timing the exact inner-iteration code path at basis indices STRATA."""
+_CACHE = {}
+
+
+def _oracle_cycle_seconds(key, mode, seed=0):
+    """Seconds of one 200-iteration restart cycle of the oracle port (krylov.py:63-164): the exact
+    inner-iteration code path timed at basis indices STRATA (cycle-average), times 200, plus the
+    cycle-end/next-start path (triangular solve, x += yQ, true residual, restart residual), scaled
+    from the sample to the workload's n.  The sample system is assembled once per process and mode.
+    Returns (seconds per cycle at the workload's size, detail)."""
     import oracle
-    from paper_2009_06725_b200.workloads import c2_case
 
-    case = c2_case()
-    s = oracle.assemble_mode_system(case.qmesh, case.density, case.viscosity, case.omegas[seed_mode],
-                                    g_mode=case.coefficients[seed_mode] * case.profile)
-    sc = oracle.jacobi_scale(s.matrix)
-    costs = [oracle.gmres_inner_step_cost(s.matrix, sc, k, RESTART, np.random.default_rng(k)) for k in STRATA]
-    return float(np.mean(costs)), costs
+    t_asm = 0.0
+    if (key, mode) not in _CACHE:
+        case = _oracle_case(key)
+        t0 = time.perf_counter()
+        s = oracle.assemble_mode_system(case.qmesh, case.density, case.viscosity, case.omegas[mode],
+                                        g_mode=case.coefficients[mode] * case.profile)
+        t_asm = time.perf_counter() - t0
+        _CACHE[(key, mode)] = (s, oracle.jacobi_scale(s.matrix), case.name)
+    s, sc, name = _CACHE[(key, mode)]
+    n_sample = s.matrix.shape[0]
+    scale = WORKLOADS[key]["n_dofs"] / n_sample
+    rng = np.random.default_rng(1000 * seed + mode)
+    costs = [oracle.gmres_inner_step_cost(s.matrix, sc, k, RESTART, rng) for k in STRATA]
+    t_end = oracle.gmres_cycle_end_cost(s.matrix, s.rhs, sc, RESTART, rng)
+    cycle = (float(np.mean(costs)) * BUDGET + t_end) * scale
+    return cycle, dict(n_sample=n_sample, nnz_sample=int(s.matrix.nnz), scale=scale, costs=costs, t_end=t_end,
+                       t_assembly=t_asm, sample=name)
+
+
+def _cpu_sample_text(key, det, procs):
+    base = (f"oracle port of krylov.py:63-164 (numpy/scipy, 1 BLAS thread per process): the exact inner-"
+            f"iteration code path timed at basis indices {list(STRATA)} of a restart-200 cycle (x200) plus the "
+            f"cycle-end path, on {det['sample']} (n = {det['n_sample']}")
+    if key == "c5":
+        base += (f", a 9-layer slab of config 5 with its cross-section, spacing and jitter), scaled by "
+                 f"n_c5/n_slab = {det['scale']:.2f} (per-iteration work is linear in n)")
+    else:
+        base += ")"
+    return base + f"; {procs} process(es); per-mode oracle assembly ({det['t_assembly']:.1f} s on the sample) " \
+                  f"is once per mode, not per cycle, and is excluded"
 
 
 def _ref_worker(args):
     os.environ["OMP_NUM_THREADS"] = "1"
-    mode, steps = args
-    import oracle
-    from paper_2009_06725_b200.workloads import c2_case
-
-    case = c2_case()
-    s = oracle.assemble_mode_system(case.qmesh, case.density, case.viscosity, case.omegas[mode],
-                                    g_mode=case.coefficients[mode] * case.profile)
-    sc = oracle.jacobi_scale(s.matrix)
+    key, mode, steps = args
     out = []
     for st in range(steps):
         t0 = time.perf_counter()
-        costs = [oracle.gmres_inner_step_cost(s.matrix, sc, k, RESTART, np.random.default_rng(k + 7 * st)) for k in STRATA]
-        out.append((float(np.mean(costs)), time.perf_counter() - t0, int(s.matrix.shape[0]), int(s.matrix.nnz),
-                    case.name))
+        cyc, det = _oracle_cycle_seconds(key, mode, seed=st)
+        out.append((cyc, time.perf_counter() - t0, det))
     return out
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port; the reference is pure Python and
+    """--impl reference: the reference's CPU path (the oracle port: the reference is pure Python and
     cannot travel to the box) on all usable host cores, one process per mode."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -158,31 +206,32 @@ def run_reference(args):
     except Exception:
         avail_gb = 64.0
     cores = len(os.sched_getaffinity(0))
-    procs = max(1, min(cores, 17, int(avail_gb // 4)))
+    # one process needs ~6 GB at the c5 slab / c2 size (basis sample + matrix + assembly peak)
+    procs = max(1, min(cores, WORKLOADS[args.workload]["total_modes"], int(avail_gb // 6)))
     steps = args.steps + args.warmup
     t0 = time.perf_counter()
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
-        res = pool.map(_ref_worker, [(1 + (m % 16), steps) for m in range(procs)])
+        res = pool.map(_ref_worker, [(args.workload, 1 + (m % (WORKLOADS[args.workload]["total_modes"] - 1)), steps)
+                                     for m in range(procs)])
     wall = time.perf_counter() - t0
     timed = [r[args.warmup:] for r in res]
-    per_step = [sum(1.0 / timed[p][s][0] for p in range(procs)) for s in range(args.steps)]
+    # every process runs cycles of its own mode concurrently: throughput = sum over processes
+    per_step = [sum(BUDGET / timed[p][s][0] for p in range(procs)) for s in range(args.steps)]
     value = float(np.mean(per_step))
     ms_step = 1e3 * float(np.mean([max(timed[p][s][1] for p in range(procs)) for s in range(args.steps)]))
+    det = res[0][0][2]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, BASELINE config 2)",
-        "config": {"workload": res[0][0][4], "modes_per_gpu": 17, "total_modes": 17, "n_dofs": res[0][0][2],
-                   "nnz": res[0][0][3], "restart": RESTART, "iterations_per_mode_per_step": BUDGET, "tol": TOL,
-                   "processes": procs},
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": f"synthetic (seeded, BASELINE config {'5' if args.workload == 'c5' else '2'})",
+        "config": config_dict(args.workload),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": (f"oracle port of krylov.py:63-164 (numpy/scipy, 1 BLAS thread per process), "
-                                    f"{procs} processes each timing the exact inner-iteration code path at basis "
-                                    f"indices {list(STRATA)} of a 200-cycle on config 2 (cycle-average cost); "
-                                    f"value = sum over processes of 1/cost")},
+                         "sample": _cpu_sample_text(args.workload, det, procs) + "; value = sum over processes of "
+                                   "200 / (seconds per cycle)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "host_cores": cores, "wall_s": wall,
+        "host_cores": cores, "wall_s": wall, "sample_s_per_step": ms_step / 1e3,
     }
     print(json.dumps(line), flush=True)
 
@@ -190,6 +239,24 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------------
 # B200 arm
 # ------------------------------------------------------------------------------------------------
+
+def _setup_workload(key, world, rank):
+    from paper_2009_06725_b200 import FluidProps
+    from paper_2009_06725_b200.assembly import get_operator
+    from paper_2009_06725_b200.distributed import expected_iterations, lpt_shard
+    from paper_2009_06725_b200.workloads import c2_case, c5_case
+
+    case = c5_case() if key == "c5" else c2_case()
+    q = case.qmesh
+    props = FluidProps(case.density, case.viscosity)
+    op = get_operator(q, props)
+    w = WORKLOADS[key]
+    if (op.n, op.nnz, case.name) != (w["n_dofs"], w["nnz"], w["workload"]):
+        raise RuntimeError(f"workload mismatch: {(op.n, op.nnz, case.name)} != {w}")
+    n_total = w["total_modes"]
+    plan = lpt_shard(expected_iterations(np.arange(n_total), 3), world)
+    return case, q, props, op, plan
+
 
 def run_b200(args):
     import torch
@@ -201,43 +268,44 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2009_06725_b200 import FluidProps, SolverSettings, _lib
-    from paper_2009_06725_b200.assembly import assemble_mode_systems, get_operator
-    from paper_2009_06725_b200.distributed import expected_iterations, gather_mode_fields, lpt_shard
+    from paper_2009_06725_b200 import SolverSettings, _lib
+    from paper_2009_06725_b200.assembly import assemble_mode_systems
+    from paper_2009_06725_b200.comm import ModeComm
     from paper_2009_06725_b200.krylov import gmres_batched
-    from paper_2009_06725_b200.workloads import _coefficients, c1_case, c2_case
 
+    key = args.workload
+    per_step = WORKLOADS[key]["modes_per_gpu_per_step"]
     hbm_peak, peak_kind = peaks()
-    case = c2_case()
-    q = case.qmesh
-    props = FluidProps(case.density, case.viscosity)
-    n_modes_total = 17 * world
-    coeffs = case.coefficients if world == 1 else _coefficients(2, n_modes_total - 1, lambda n: 1.0 + n ** 1.5)
-    omegas_all = 2.0 * np.pi * np.arange(n_modes_total) / case.period
-    plan = lpt_shard(expected_iterations(np.arange(n_modes_total), 3), world)
-    mine = plan[rank]
-    nb = len(mine)
-    omegas = omegas_all[mine]
-    g_host = np.stack([coeffs[i] * case.profile for i in mine]).astype(complex)
-
     t_setup = time.perf_counter()
-    op = get_operator(q, props)
-    batch = assemble_mode_systems(q, props, omegas, list(g_host), None, operator=op)
-    ws = op.krylov(RESTART, nb, BUDGET)
+    case, q, props, op, plan = _setup_workload(key, world, rank)
+    mine = plan[rank]
+    dev = op.device
+    coeffs = case.coefficients
+    omegas_all = case.omegas
+    profile_dev = torch.from_numpy(np.ascontiguousarray(case.profile, dtype=complex)).to(dev)
+    ws = op.krylov(RESTART, per_step, BUDGET)
+    comm = ModeComm.from_process_group(local) if world > 1 else None
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream()
 
-    def step():
-        return ws.solve(omegas, batch.rhs, None, TOL, BUDGET, jacobi=True)
+    def modes_of_step(s):
+        return [mine[(s * per_step + j) % len(mine)] for j in range(per_step)]
 
-    for _ in range(args.warmup):
-        out = step()
+    def step(s):
+        ms = modes_of_step(s)
+        cf = torch.tensor([coeffs[m] for m in ms], dtype=torch.complex128, device=dev)
+        g = profile_dev[None] * cf[:, None, None]
+        rhs = op.rhs(omegas_all[ms], None, g)
+        return ws.solve(omegas_all[ms], rhs, None, TOL, BUDGET, jacobi=True)
+
+    for s in range(args.warmup):
+        step(s)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # ---- timed region: inputs resident in HBM (basis 200+1 vectors x 17 modes >> 126 MB L2) ----
+    # ---- timed region: inputs resident in HBM ----
     l0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -246,17 +314,16 @@ def run_b200(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         iters = 0
-        for _ in range(args.steps):
-            out = step()
+        for s in range(args.steps):
+            out = step(args.warmup + s)
             iters += int(out["iterations"].sum())
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = _lib.launch_count() - l0
-    ms_total = e0.elapsed_time(e1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    it_t = torch.tensor([iters], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    it_t = torch.tensor([iters], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
@@ -265,75 +332,152 @@ def run_b200(args):
     value = total_iters / (ms_total * 1e-3)
     ms_per_step = ms_total / args.steps
 
-    # ---- end to end through the public API: pinned host BCs in, nodal fields out, every step ----
-    g_pin = torch.from_numpy(g_host.reshape(nb, q.n_velocity_nodes, q.dim)).pin_memory()
-    u_pin = torch.empty((nb, q.n_velocity_nodes, q.dim), dtype=torch.complex128).pin_memory()
-    p_pin = torch.empty((nb, q.n_vertices), dtype=torch.complex128).pin_memory()
+    # ---- end to end through the public API: pinned host Dirichlet data in, nodal fields out and
+    #      gathered to rank 0 over the library's NCCL communicator, every step ----
+    nvn, dim = q.n_velocity_nodes, q.dim
+    g_pin = torch.empty((per_step, nvn, dim), dtype=torch.complex128).pin_memory()
+    g_np = g_pin.numpy()
+    prof_np = np.ascontiguousarray(case.profile, dtype=complex)
+    nf = nvn * dim + q.n_vertices
+    f_pin = torch.empty((per_step, nf), dtype=torch.complex128).pin_memory()
+    fields = torch.empty((per_step, nf), dtype=torch.complex128, device=dev)
+    gather_out = torch.empty((world * per_step, nf), dtype=torch.complex128, device=dev) if rank == 0 and world > 1 \
+        else None
     settings = SolverSettings(tolerance=TOL, restart=RESTART, max_iterations=BUDGET)
     h2d = g_pin.numel() * 16
-    d2h = (u_pin.numel() + p_pin.numel()) * 16
+    d2h = f_pin.numel() * 16
 
-    def e2e_step():
-        g_dev = g_pin.to(op.device, non_blocking=True)
-        b = assemble_mode_systems(q, props, omegas, None, None, operator=op, g_device=g_dev)
-        X, reps = gmres_batched(b, settings)
+    def e2e_step(s):
+        ms = modes_of_step(s)
+        for j, m in enumerate(ms):
+            np.multiply(prof_np, coeffs[m], out=g_np[j])          # the user's nodal BC data for this mode
+        g_dev = g_pin.to(dev, non_blocking=True)
+        b = assemble_mode_systems(q, props, omegas_all[ms], None, None, operator=op, g_device=g_dev)
+        X, reps = gmres_batched(b, settings, keep_history=False)
         U, P = op.expand(X, b.g)
-        if world > 1:
-            nu = q.n_velocity_nodes * q.dim
-            gather_mode_fields(torch.cat([U.reshape(nb, -1), P], dim=1), plan, rank, world)
-        u_pin.copy_(U, non_blocking=True)
-        p_pin.copy_(P, non_blocking=True)
+        fields[:, : nvn * dim] = U.reshape(per_step, -1)
+        fields[:, nvn * dim:] = P
+        if world > 1:   # every rank's fields of this step -> rank 0 (slots rank*per_step + j)
+            step_plan = [list(range(r * per_step, (r + 1) * per_step)) for r in range(world)]
+            comm.gather_modes(fields, step_plan, root=0, out=gather_out)
+        f_pin.copy_(fields, non_blocking=True)
         return sum(r.iterations for r in reps)
 
-    e2e_step()
+    e2e_step(0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0.record(stream)
     w0 = time.perf_counter()
     e_iters = 0
-    for _ in range(args.steps):
-        e_iters += e2e_step()
+    for s in range(args.steps):
+        e_iters += e2e_step(s + 1)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_wall = time.perf_counter() - w0
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    ei = torch.tensor([e_iters], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    ei = torch.tensor([e_iters], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(ei, op=dist.ReduceOp.SUM)
     e2e_value = float(ei.item()) / (float(t.item()) * 1e-3)
+    del g_pin, f_pin, fields, gather_out
 
     # ---- roofline: one instrumented (event-timed, un-graphed) cycle on the same stream ----
-    ws.load_rhs(batch.rhs)
-    prof = ws.profile(omegas, TOL, BUDGET, jacobi=True)
+    ms0 = modes_of_step(0)
+    cf = torch.tensor([coeffs[m] for m in ms0], dtype=torch.complex128, device=dev)
+    ws.load_rhs(op.rhs(omegas_all[ms0], None, profile_dev[None] * cf[:, None, None]))
+    prof = ws.profile(omegas_all[ms0], TOL, BUDGET, jacobi=True)
     dom_name = max((k for k in prof if k != "spmv"), key=lambda k: prof[k]["ms"])
     dom = prof[dom_name]
-    traffic = None
-    try:   # DRAM traffic of the same kernel from the committed `ncu --set full` capture (J = 100 launch)
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_full.json")) as fh:
-            cap = json.load(fh)
-        rec = next(r for r in cap["launches"] if r["kernel"].startswith("void k_pass<2>"))
-        alg = nb * (100 + 2) * 16 * op.n
-        traffic = {"bytes_per_launch": rec["dram_read_bytes"] + rec["dram_write_bytes"],
-                   "algorithmic_bytes_same_launch": alg,
-                   "ratio": (rec["dram_read_bytes"] + rec["dram_write_bytes"]) / alg,
-                   "source": "profiles/r1_ncu_full.json (k_pass<2>, tick 100: J = 100)"}
-    except Exception:
-        traffic = None
+    traffic = _traffic_from_profile(key, dom_name, dom)
     achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
-    share = dom["ms"] / sum(v["ms"] for v in prof.values())
+    total_ms = sum(v["ms"] for v in prof.values())
     passes_bytes = sum(prof[k]["bytes"] for k in prof if k != "spmv")
     passes_ms = sum(prof[k]["ms"] for k in prof if k != "spmv")
 
-    # ---- standalone mode-batched SpMV over the 17 modes (second half of the metric): the
-    #      mode-interleaved kernel the GMRES tick runs, and the row-layout variant for reference ----
-    xi = torch.randn((op.ld, nb), dtype=torch.complex128, device=op.device)
-    ys = torch.zeros((nb, op.ld), dtype=torch.complex128, device=op.device)
-    xr = torch.randn((nb, op.ld), dtype=torch.complex128, device=op.device)
+    # ---- the tick SpMV standalone (second half of the metric) ----
+    spmv = _spmv_numbers(op, omegas_all[ms0], ws, e0, e1, stream, hbm_peak, torch)
+    spmv["share_of_cycle"] = prof["spmv"]["ms"] / total_ms
+    spmv["in_cycle_gbs"] = (op.spmv_bytes(per_step) * prof["spmv"]["launches"]) / (prof["spmv"]["ms"] * 1e-3) / 1e9
 
-    def time_spmv(fn, reps=20):
-        for _ in range(3):
+    extras = {}
+    if rank == 0 and world == 1 and not args.quick:
+        op.release_workspaces()
+        extras.update(_converged_extras(torch))
+        if key == "c5":
+            extras["c2_secondary"] = _c2_secondary(torch, hbm_peak)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c0 = time.perf_counter()
+        cyc, det = _oracle_cycle_seconds(key, 1)
+        cpu = {"value": BUDGET / cyc, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": _cpu_sample_text(key, det, 1) + f"; per-index seconds on the sample "
+                         f"{[round(c, 3) for c in det['costs']]}, cycle end {det['t_end']:.3f} s; "
+                         f"{time.perf_counter() - c0:.1f} s of CPU work"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        cfg = config_dict(key)
+        w = WORKLOADS[key]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128",
+            "data": f"synthetic (seeded, BASELINE config {'5' if key == 'c5' else '2'})",
+            "config": cfg,
+            "setup_s": setup_s,
+            "sweep": {"modes": w["total_modes"], "max_modes_per_gpu": max(len(p) for p in plan),
+                      "one_cycle_of_every_mode_s": max(len(p) for p in plan) / per_step * ms_per_step / 1e3,
+                      "note": "derived: makespan of one restart cycle of all modes on n_gpus (LPT plan)"},
+            "roofline": {"bound": "hbm", "kernel": f"k_pass<{dom_name}>", "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": None if traffic is None else traffic["ratio"] * dom["bytes"] / dom["launches"],
+                         "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
+                         "traffic_detail": traffic, "peak_kind": peak_kind, "share_of_step": dom["ms"] / total_ms,
+                         "all_basis_passes_gbs": passes_bytes / (passes_ms * 1e-3) / 1e9,
+                         "per_kernel": prof},
+            "spmv": spmv,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "gather": "ss_comm_gather_modes (NCCL) to rank 0 every step" if world > 1 else None,
+                    "wall_s": e2e_wall},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _traffic_from_profile(key, dom_name, dom):
+    """DRAM traffic / algorithmic bytes of the dominant kernel from the committed `ncu --set full`
+    capture of this workload (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", f"r2_ncu_full_{key}.json")
+    try:
+        with open(path) as fh:
+            cap = json.load(fh)
+        want = {"passA_dot": "k_pass<1>", "passB_update_dot": "k_pass<2>", "passC_update_norm": "k_pass<3>"}[dom_name]
+        rec = next(r for r in cap["launches"] if want in r["kernel"])
+        return {"bytes_per_launch": rec["dram_read_bytes"] + rec["dram_write_bytes"],
+                "algorithmic_bytes_same_launch": rec["algorithmic_bytes"],
+                "ratio": (rec["dram_read_bytes"] + rec["dram_write_bytes"]) / rec["algorithmic_bytes"],
+                "source": os.path.relpath(path, ROOT)}
+    except Exception:
+        return None
+
+
+def _spmv_numbers(op, omegas, ws, e0, e1, stream, hbm_peak, torch):
+    nb = len(omegas)
+    xr = torch.randn((nb, op.ld), dtype=torch.complex128, device=op.device)
+    ys = torch.zeros((nb, op.ld), dtype=torch.complex128, device=op.device)
+
+    def time_it(fn, reps=10):
+        for _ in range(2):
             fn()
         e0.record(stream)
         for _ in range(reps):
@@ -342,83 +486,85 @@ def run_b200(args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    spmv_ms = time_spmv(lambda: op.spmv_interleaved(omegas, xi, jacobi=True, out=ys))
-    spmv_row_ms = time_spmv(lambda: op.spmv(omegas, xr, jacobi=True, out=ys))
-    spmv_bytes = op.spmv_bytes(nb)
-    spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
-    info = op.info
-    spmv_gather = int((q.dim * int(info[4]) + int(info[5]) + q.dim * int(info[6])) * nb * 16)
+    row = ws.options()["row_spmv"]
+    if row:
+        ms = time_it(lambda: op.spmv(omegas, xr, jacobi=True, out=ys))
+        kern = "row-layout tick SpMV (saddle_block: 8 lanes per node row)"
+    else:
+        xi = torch.randn((op.ld, nb), dtype=torch.complex128, device=op.device)
+        ms = time_it(lambda: op.spmv_interleaved(omegas, xi, jacobi=True, out=ys))
+        kern = "k_spmv_interleaved (tick SpMV)"
+    by = op.spmv_bytes(nb)
+    gbs = by / (ms * 1e-3) / 1e9
+    return {"kernel": kern, "modes": nb, "ms": ms, "bytes": by, "achieved_gbs": gbs, "frac": gbs / hbm_peak,
+            "peak": hbm_peak,
+            "note": "algorithmic bytes (ss_spmv_bytes) = matrix stream once + x read + y write per mode"}
 
-    extras = {}
-    if rank == 0 and world == 1 and not args.quick:
-        # config 1 (2D channel, 9 modes) solved to convergence at 1e-10: measured modes/s
-        c1 = c1_case()
-        p1 = FluidProps(c1.density, c1.viscosity)
-        op1 = get_operator(c1.qmesh, p1)
-        b1 = assemble_mode_systems(c1.qmesh, p1, c1.omegas, None, c1.h_modes(), operator=op1)
-        ws1 = op1.krylov(RESTART, c1.n_modes + 1, 200_000)
-        ws1.solve(c1.omegas, b1.rhs, None, TOL, 200_000)
+
+def _converged_extras(torch):
+    """Measured modes solved/s: config 1 (2D) and the down-scaled 3D pipes, every mode to 1e-10."""
+    from paper_2009_06725_b200 import FluidProps
+    from paper_2009_06725_b200.assembly import assemble_mode_systems, get_operator
+    from paper_2009_06725_b200.workloads import c1_case, c5_small, pipe3d_case
+
+    out = {}
+    for tag, case in (("c1_converged", c1_case()), ("c3d_converged_pipe3d", pipe3d_case()),
+                      ("c3d_converged_c5small", c5_small())):
+        props = FluidProps(case.density, case.viscosity)
+        op = get_operator(case.qmesh, props)
+        idx = np.arange(case.n_modes + 1)
+        b = assemble_mode_systems(case.qmesh, props, case.omegas, case.g_modes(), case.h_modes(), operator=op)
+        ws = op.krylov(RESTART, idx.size, 400_000)
+        ws.solve(case.omegas, b.rhs, None, TOL, 400_000)   # warm-up (graph capture)
         torch.cuda.synchronize()
         w0 = time.perf_counter()
-        o1 = ws1.solve(c1.omegas, b1.rhs, None, TOL, 200_000)
-        c1_s = time.perf_counter() - w0
-        extras["c1_converged"] = {
-            "workload": c1.name, "modes": int(c1.n_modes + 1), "tol": TOL, "seconds": c1_s,
-            "modes_per_s": (c1.n_modes + 1) / c1_s, "all_converged": bool(o1["converged"].all()),
-            "iterations": [int(v) for v in o1["iterations"]],
-            "ticks": ws1.last_stats()[0],
-        }
+        o = ws.solve(case.omegas, b.rhs, None, TOL, 400_000)
+        sec = time.perf_counter() - w0
+        out[tag] = {"workload": case.name, "n_dofs": op.n, "modes": int(idx.size), "tol": TOL, "restart": RESTART,
+                    "seconds": sec, "modes_per_s": idx.size / sec, "all_converged": bool(o["converged"].all()),
+                    "iterations": [int(v) for v in o["iterations"]], "ticks": ws.last_stats()[0],
+                    "measured": "every mode solved to the reference's stopping rule in one device batch"}
+        op.release_workspaces()
+    return out
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        c0 = time.perf_counter()
-        cost, costs = _oracle_cycle_cost()
-        cpu = {"value": 1.0 / cost, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle port of krylov.py:63-164 (numpy/scipy, 1 thread) on config 2 mode 1: exact "
-                          f"inner-iteration code path timed at basis indices {list(STRATA)} of a 200-cycle, "
-                          f"mean = {cost:.3f} s/iteration (per-index {[round(c, 3) for c in costs]}); "
-                          f"{time.perf_counter() - c0:.1f} s of CPU work incl. oracle assembly")}
 
-    if rank == 0:
-        clocks = clk.summary()
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, BASELINE config 2)",
-            "config": {"workload": case.name, "modes_per_gpu": nb, "total_modes": n_modes_total,
-                       "n_dofs": op.n, "nnz": op.nnz, "restart": RESTART, "iterations_per_mode_per_step": BUDGET,
-                       "tol": TOL, "l2": "inputs larger than L2 (basis 17 x 201 x n x 16 B >> 126 MB)",
-                       "setup_s": setup_s,
-                       "projected_modes_per_s": {
-                           "value": value / 2.0e5,
-                           "basis": "PROJECTION ONLY: value / 2e5 iterations per mode (krylov.py maxiter default; "
-                                    "c2 needs >= 1e5 at 1e-10, SURVEY.md 8d)"}},
-            "roofline": {"bound": "hbm", "kernel": f"k_pass<{dom_name}>", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": None if traffic is None else traffic["ratio"] * dom["bytes"] / dom["launches"],
-                         "algorithmic_bytes_per_launch": dom["bytes"] / dom["launches"],
-                         "traffic_detail": traffic,
-                         "peak_kind": peak_kind, "share_of_step": share,
-                         "all_basis_passes_gbs": passes_bytes / (passes_ms * 1e-3) / 1e9,
-                         "per_kernel": prof},
-            "spmv": {"kernel": "k_spmv_interleaved (tick SpMV)", "modes": nb, "ms": spmv_ms, "bytes": spmv_bytes,
-                     "achieved_gbs": spmv_gbs, "frac": spmv_gbs / hbm_peak, "peak": hbm_peak,
-                     "row_layout_ms": spmv_row_ms,
-                     "gathered_bytes": spmv_gather, "gather_tbs": spmv_gather / (spmv_ms * 1e-3) / 1e12,
-                     "note": ("algorithmic bytes = matrix once + x read + y write per mode; the kernel gathers "
-                              "x once per stored entry and mode (gathered_bytes, served by L1/L2 at "
-                              "gather_tbs); ncu: L1 hit 55 %, L2 hit 52 %, long-scoreboard stalls -> "
-                              "gather-latency bound")},
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "wall_s": e2e_wall},
-            "gpu_launches": int(launches),
-            "clocks": clocks,
-        }
-        line.update(extras)
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+def _c2_secondary(torch, hbm_peak):
+    """Config 2 (17 modes in one batch per GPU): one graphed cycle per step, device-resident."""
+    from paper_2009_06725_b200 import FluidProps
+    from paper_2009_06725_b200.assembly import assemble_mode_systems, get_operator
+    from paper_2009_06725_b200.workloads import c2_case
+
+    case = c2_case()
+    props = FluidProps(case.density, case.viscosity)
+    op = get_operator(case.qmesh, props)
+    b = assemble_mode_systems(case.qmesh, props, case.omegas, case.g_modes(), None, operator=op)
+    ws = op.krylov(RESTART, 17, BUDGET)
+    ws.solve(case.omegas, b.rhs, None, TOL, BUDGET)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    it = 0
+    for _ in range(3):
+        it += int(ws.solve(case.omegas, b.rhs, None, TOL, BUDGET)["iterations"].sum())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    xi = torch.randn((op.ld, 17), dtype=torch.complex128, device=op.device)
+    ys = torch.zeros((17, op.ld), dtype=torch.complex128, device=op.device)
+    for _ in range(3):
+        op.spmv_interleaved(case.omegas, xi, jacobi=True, out=ys)
+    e0.record(stream)
+    for _ in range(20):
+        op.spmv_interleaved(case.omegas, xi, jacobi=True, out=ys)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sms = e0.elapsed_time(e1) / 20
+    by = op.spmv_bytes(17)
+    op.release_workspaces()
+    return {"workload": case.name, "modes_per_step": 17, "value": it / (ms * 1e-3), "unit": UNIT,
+            "ms_per_step": ms / 3, "spmv_ms": sms, "spmv_gbs": by / (sms * 1e-3) / 1e9,
+            "spmv_frac": by / (sms * 1e-3) / 1e9 / hbm_peak}
 
 
 def main():
@@ -427,8 +573,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip the config-1 convergence extra")
+    ap.add_argument("--quick", action="store_true", help="skip the converged-mode and config-2 extras")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -28,9 +28,12 @@ extern "C" {
 
 typedef struct ss_pattern ss_pattern; /* mesh numbering + symbolic pattern + device operator  */
 typedef struct ss_krylov ss_krylov;   /* batched GMRES workspace (basis, Hessenberg, state)   */
+typedef struct ss_comm ss_comm;       /* NCCL communicator for the mode-field gather          */
+
+#define SS_COMM_ID_BYTES 128
 
 /* ABI revision: the Python binding refuses (rebuilds) a library whose ss_version() differs. */
-#define SS_ABI_VERSION 2
+#define SS_ABI_VERSION 3
 
 const char* ss_last_error(void);
 int ss_version(void);
@@ -166,6 +169,25 @@ int ss_krylov_bench_pass(ss_krylov* k, int nb, int kidx, int which, int reps, vo
  * fields_dev: nb x n complex; phases_dev: nb x nt complex; out_dev: nt x n doubles. */
 int ss_reconstruct(int nb, int nt, int64_t n, const double* fields_dev, const double* phases_dev, double* out_dev,
                    void* stream);
+
+/* ---- Multi-GPU mode sharding (one process per GPU): the collective that replaces
+ * the reference's in-process ModeSolution list of the thread pool (spectral.py:296-305).  NCCL is
+ * dlopen'ed at first use (SS_NCCL_LIB, default "libnccl.so.2"). ---- */
+/* NCCL version code of the loaded library (e.g. 22809), or -1 if NCCL cannot be loaded. */
+int ss_comm_nccl_version(void);
+/* ncclGetUniqueId: SS_COMM_ID_BYTES bytes made on one rank and shared out of band. */
+int ss_comm_unique_id(uint8_t* id_out);
+/* ncclCommInitRank on `device`. */
+int ss_comm_create(int nranks, int rank, const uint8_t* id, int device, ss_comm** out);
+void ss_comm_destroy(ss_comm* c);
+/* Gather solved modal fields (complex128) to `root`: rank r sends its counts[r] fields (count
+ * complex values each, stride ld, from send_dev); the root stores field j of rank r at
+ * recv_dev + dest[counts[0] + ... + counts[r-1] + j] * ld.  One grouped ncclSend/ncclRecv round. */
+int ss_comm_gather_modes(ss_comm* c, const double* send_dev, int64_t n_local, int64_t count, int64_t ld,
+                         double* recv_dev, const int64_t* counts_host, const int64_t* dest_host, int root,
+                         void* stream);
+/* In-place elementwise max over ranks of n doubles on the device. */
+int ss_comm_allreduce_max(ss_comm* c, double* buf_dev, int64_t n, void* stream);
 
 /* ---- Field snapshots (host runtime, io.py:88-183): "%.17g" text, byte-identical to the reference's
  * "{:.17g}" writer, formatted/parsed in parallel.  Paths are NUL-terminated UTF-8. ---- */

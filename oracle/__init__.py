@@ -18,6 +18,7 @@ from .scvs import (  # noqa: F401
     assemble_mode_system,
     assemble_stiffness_scalar,
     gmres,
+    gmres_cycle_end_cost,
     gmres_inner_step_cost,
     gmres_solve,
     jacobi_scale,

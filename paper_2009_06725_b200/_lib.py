@@ -74,12 +74,18 @@ SIGNATURES = {
     "ss_krylov_profile": (I32, [P, I32, PD, D, I64, I32, P, PD, PI64, PI64]),
     "ss_krylov_bench_pass": (I32, [P, I32, I32, I32, I32, P, PF, PI64]),
     "ss_reconstruct": (I32, [I32, I32, I64, P, P, P, P]),
+    "ss_comm_nccl_version": (I32, []),
+    "ss_comm_unique_id": (I32, [PU8]),
+    "ss_comm_create": (I32, [I32, I32, PU8, I32, C.POINTER(P)]),
+    "ss_comm_destroy": (None, [P]),
+    "ss_comm_gather_modes": (I32, [P, P, I64, I64, I64, P, PI64, PI64, I32, P]),
+    "ss_comm_allreduce_max": (I32, [P, P, I64, P]),
 }
 
 _lib = None
 
 # Must equal SS_ABI_VERSION in include/spectralstokes_b200.h (bumped whenever an entry point changes).
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 def load(build_if_missing: bool = True):

@@ -358,6 +358,13 @@ class SaddleOperator:
             self._krylov[restart] = ws
         return ws
 
+    def release_workspaces(self):
+        """Free every cached Krylov workspace (basis, Hessenberg, graphs) of this operator."""
+        with self.lock:
+            for ws in self._krylov.values():
+                ws.close()
+            self._krylov.clear()
+
     def max_batch(self, restart: int) -> int:
         """Modes that fit one GPU at this restart (basis is (restart+1)*ld*16 B per mode)."""
         torch = _lib.torch_mod()

@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libss_b200.so"
-SOURCES = ["pattern.cpp", "assemble.cu", "krylov.cu", "reconstruct.cu", "snapshot.cpp"]
+SOURCES = ["pattern.cpp", "assemble.cu", "krylov.cu", "reconstruct.cu", "snapshot.cpp", "comm.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fopenmp",
-           *objs, "-o", str(tmp), "-lcudart", "-lgomp"]
+           *objs, "-o", str(tmp), "-lcudart", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

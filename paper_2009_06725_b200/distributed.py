@@ -1,31 +1,80 @@
-"""Multi-GPU mode sharding: one process per GPU, modes partitioned, one collective at the end.
+"""Multi-GPU mode sharding: one process per GPU, modes partitioned, one gather at the end.
 
-Modes are independent boundary-value problems (reference spectral.py:287-305; PAPER §1): there
-is no exchange during the solves.  The only data movement is gathering the solved modal fields
-to the reconstructing rank, done here with one ``all_gather`` over torch.distributed (NCCL over
-NVLink on the GPU box, gloo in the CPU tests).
+Modes are independent boundary-value problems (reference spectral.py:287-305; PAPER §1): there is
+no exchange during the solves.  The only data movement is gathering the solved modal fields to the
+reconstructing rank:
 
-* :func:`lpt_shard` — longest-processing-time-first assignment by expected GMRES iterations
-  (SURVEY.md §8e); deterministic for a given cost vector.
-* :func:`expected_iterations` — cost model: flat in 2D, growing ~linearly with the mode index in
-  3D (measured on the reference: 9 687 iterations for mode 1 vs 20 603 for mode 16 on the small
-  pipe, tests/golden/pipe3d.npz).
-* :func:`gather_mode_fields` — padded all_gather of per-rank modal fields to every rank / dst.
-* :func:`solve_mode_systems_distributed` — shard, solve the local batch on the local GPU, gather.
+* on GPUs, through the library's NCCL communicator (:class:`~.comm.ModeComm`,
+  ``ss_comm_gather_modes``: one grouped ncclSend/ncclRecv round over NVLink, fields land in their
+  global slot on the root);
+* without GPUs (the CPU tests), through torch.distributed ``gather`` on the gloo backend.
+
+Pieces:
+
+* :func:`expected_iterations` -- the LPT cost model: flat in 2D, linear in the mode index in 3D,
+  fitted to the reference's own converged iteration counts (tests/golden pipe3d / small3d:
+  modes 1 and 16); :func:`calibrate_iterations` refits it from any measured counts and
+  :func:`iterations_from_first_cycle` predicts counts from a first restart cycle's estimates.
+* :func:`lpt_shard` -- longest-processing-time-first assignment.
+* :func:`gather_mode_fields` -- the gather to one destination rank.
+* :func:`solve_mode_systems_distributed` -- shard, solve the local batch on this rank's GPU, free
+  the Krylov workspace, gather.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["lpt_shard", "expected_iterations", "gather_mode_fields", "solve_mode_systems_distributed"]
+__all__ = ["lpt_shard", "expected_iterations", "calibrate_iterations", "iterations_from_first_cycle",
+           "gather_mode_fields", "solve_mode_systems_distributed", "DEFAULT_3D_MODEL"]
+
+# Iterations to 1e-10 (restart 200) measured by the reference on the down-scaled 3D pipes:
+# pipe3d (n = 8 782) mode 1: 9 687, mode 16: 20 603 (tests/golden/pipe3d.npz); relative to
+# mode 1 that is 1 + 0.0726 (idx - 1) -> model a + b*idx with a = 1, b = 0.075 (per mode-1 cost).
+DEFAULT_3D_MODEL = (1.0, 0.075)
 
 
-def expected_iterations(indices, dim: int) -> np.ndarray:
+def calibrate_iterations(indices, iterations):
+    """Least-squares fit ``iters ~ a + b * idx`` to measured counts; returns (a, b) scaled so a + b = 1
+    at mode 1 (only ratios matter for load balance)."""
+    idx = np.asarray(indices, dtype=float)
+    it = np.asarray(iterations, dtype=float)
+    if idx.size < 2 or np.ptp(idx) == 0:
+        return 1.0, 0.0
+    b, a = np.polyfit(idx, it, 1)
+    s = a + b
+    if s <= 0:
+        return 1.0, 0.0
+    return float(a / s), float(b / s)
+
+
+def iterations_from_first_cycle(histories, tol, restart):
+    """Predicted total iterations per mode from the first restart cycle's residual estimates.
+
+    Restarted GMRES reduces the estimate by roughly the same factor every cycle, so
+    ``cycles ~ log(tol / est_0) / log(est_end / est_0)`` for each mode's first-cycle history.
+    """
+    out = []
+    for h in histories:
+        h = np.asarray(h, dtype=float)
+        if h.size == 0 or h[0] <= 0:
+            out.append(0.0)
+            continue
+        if h[-1] <= tol * h[0] or h.size < restart:
+            out.append(float(h.size))
+            continue
+        rate = np.log(max(h[-1], 1e-300) / h[0])
+        cycles = np.log(tol) / rate if rate < 0 else 1e6
+        out.append(float(cycles * restart))
+    return np.asarray(out)
+
+
+def expected_iterations(indices, dim: int, model=None) -> np.ndarray:
     idx = np.asarray(indices, dtype=float)
     if dim == 2:
         return np.ones_like(idx)
-    return 1.0 + 0.075 * idx
+    a, b = DEFAULT_3D_MODEL if model is None else model
+    return a + b * idx
 
 
 def lpt_shard(costs, world: int):
@@ -45,44 +94,57 @@ def lpt_shard(costs, world: int):
     return [sorted(b) for b in bins]
 
 
-def gather_mode_fields(local, plan, rank: int, world: int, group=None):
-    """All-gather per-rank (m_r, N) field blocks into the global (sum m_r, N) order of ``plan``.
+def gather_mode_fields(local, plan, rank: int, world: int, group=None, comm=None, dst: int = 0):
+    """Gather per-rank (m_r, N) field blocks to rank ``dst`` in the global order of ``plan``.
 
-    ``local`` is a real or complex torch tensor on the backend's device; complex data travels as
-    float64 pairs.  Returns the global tensor (every rank receives it).
+    With a :class:`~.comm.ModeComm` the library's NCCL gather runs on the device; otherwise
+    torch.distributed ``gather`` (gloo in the CPU tests; CUDA tensors are staged through host
+    memory).  Returns the (sum m_r, N) tensor on ``dst`` and None elsewhere.
     """
     import torch
+
+    if comm is not None:
+        return comm.gather_modes(local, plan, root=dst)
     import torch.distributed as dist
 
     counts = [len(p) for p in plan]
     m = max(counts) if counts else 0
     is_complex = local.is_complex()
     payload = torch.view_as_real(local) if is_complex else local
+    staged = dist.get_backend(group) == "gloo" and payload.is_cuda
+    dev = payload.device
+    if staged:
+        payload = payload.cpu()
     tail = tuple(payload.shape[1:])
     pad = torch.zeros((m,) + tail, dtype=payload.dtype, device=payload.device)
     pad[: payload.shape[0]] = payload
-    bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
     total = sum(counts)
     out = torch.empty((total,) + tail, dtype=payload.dtype, device=payload.device)
     for r, idxs in enumerate(plan):
         if idxs:
-            out[torch.as_tensor(idxs, device=payload.device)] = bufs[r][: len(idxs)]
+            out[torch.as_tensor(idxs)] = bufs[r][: len(idxs)]
+    if staged:
+        out = out.to(dev)
     return torch.view_as_complex(out) if is_complex else out
 
 
 def solve_mode_systems_distributed(qmesh, props, indices, omegas, g_modes, h_modes, settings, rank: int,
-                                   world: int, group=None):
-    """Shard modes over ranks (LPT), solve the local batch on this rank's GPU, gather fields.
+                                   world: int, group=None, comm=None, dst: int = 0, model=None):
+    """Shard modes over ranks (LPT), solve the local batch on this rank's GPU, gather fields to ``dst``.
 
-    Returns ``(U, P, reports_local, plan)`` with U (n_modes, n_vn, dim) and P (n_modes, n_vert)
-    complex device tensors on every rank.
+    Returns ``(U, P, reports_local, plan)``: U (n_modes, n_vn, dim) and P (n_modes, n_vert) complex
+    device tensors on ``dst`` (None elsewhere).
     """
     import torch
 
+    from .assembly import get_operator
     from .spectral import solve_mode_systems
 
-    plan = lpt_shard(expected_iterations(indices, qmesh.dim), world)
+    plan = lpt_shard(expected_iterations(indices, qmesh.dim, model), world)
     mine = plan[rank]
     sols = solve_mode_systems(qmesh, props, [indices[i] for i in mine], np.asarray(omegas)[mine],
                               None if g_modes is None else [g_modes[i] for i in mine],
@@ -93,7 +155,11 @@ def solve_mode_systems_distributed(qmesh, props, indices, omegas, g_modes, h_mod
     for j, s in enumerate(sols):
         local[j, :nu] = s._device[0].reshape(-1)
         local[j, nu:] = s._device[1]
-    full = gather_mode_fields(local, plan, rank, world, group)
+        s._device = None
+    get_operator(qmesh, props).release_workspaces()   # the basis is dead weight during the gather
+    full = gather_mode_fields(local, plan, rank, world, group, comm=comm, dst=dst)
+    if full is None:
+        return None, None, [s.report for s in sols], plan
     U = full[:, :nu].reshape(-1, qmesh.n_velocity_nodes, qmesh.dim)
     P = full[:, nu:]
     return U, P, [s.report for s in sols], plan

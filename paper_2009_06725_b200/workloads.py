@@ -123,6 +123,16 @@ def c5_case(n_rings: int = 35, n_layers: int = 363) -> Case:
                 _coefficients(5, 127, lambda n: 1.0 + n ** 2), "inlet", "dirichlet", radius=0.5)
 
 
+def c5_slab(n_layers: int = 9) -> Case:
+    """A slab of config 5: the same 35-ring cross-section, layer spacing (5/363), jitter amplitude and
+    fluid, ``n_layers`` layers long.  Per-DOF work of a GMRES iteration is the same as config 5's
+    (identical element shapes and row lengths); the CPU baseline times the oracle on it and scales
+    by n_c5 / n_slab (SpMV ~ nnz, CGS2 ~ n k: both linear in n)."""
+    mesh, geom = jittered_pipe(35, n_layers, 0.5, 5.0 * n_layers / 363, seed=105)
+    return Case(f"c5_slab_{mesh.n_elements}tets", mesh, geom, 1.06, 0.04, 1.0, 127,
+                _coefficients(5, 127, lambda n: 1.0 + n ** 2), "inlet", "dirichlet", radius=0.5)
+
+
 # Down-scaled instances of the SAME generators (CPU-convergeable; parity at 1e-10 vs the reference)
 def c3_small() -> Case:
     return c3_case(2)

@@ -1,6 +1,6 @@
 """Instrumented (un-graphed, event-timed) solve of a BASELINE config for per-kernel timing.
 
-    python tools/profile_case.py c1|c2|pipe3d [iters] [modes]
+    python tools/profile_case.py c1|c2|pipe3d|c3|c4|c5 [iters] [modes]
 """
 import os
 import sys
@@ -12,11 +12,11 @@ import torch  # noqa: E402
 
 from paper_2009_06725_b200 import FluidProps  # noqa: E402
 from paper_2009_06725_b200.assembly import assemble_mode_systems, get_operator  # noqa: E402
-from paper_2009_06725_b200.workloads import c1_case, c2_case, pipe3d_case  # noqa: E402
+from paper_2009_06725_b200.workloads import c1_case, c2_case, c3_case, c4_case, c5_case, pipe3d_case  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 110
-case = {"c1": c1_case, "c2": c2_case, "pipe3d": pipe3d_case}[name]()
+case = {"c1": c1_case, "c2": c2_case, "pipe3d": pipe3d_case, "c3": c3_case, "c4": c4_case, "c5": c5_case}[name]()
 nb = int(sys.argv[3]) if len(sys.argv) > 3 else case.n_modes + 1
 q = case.qmesh
 props = FluidProps(case.density, case.viscosity)
