@@ -8,7 +8,9 @@
 // scattered through the precomputed element->slot map, one colour per launch (elements of a
 // colour share no vertex, so no two threads touch the same slot: atomic-free and deterministic).
 // It runs ONCE per mesh; the reference re-assembles per mode (spectral.py:280).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ss_common.h"
@@ -433,11 +435,48 @@ __global__ void __launch_bounds__(256) k_spmv_saddle(SsOperatorDev op, int nb, c
   }
 }
 
+// The same product with the TMA-staged row-layout streamer (persistent CTAs; each staged chunk of
+// the matrix is applied to all nb modes while it sits in shared memory).
+template <int DIM>
+__global__ void __launch_bounds__(256, 2) k_spmv_stream(SsOperatorDev op, int nb, const double* __restrict__ omegas,
+                                                     const double2* __restrict__ X, double2* __restrict__ Y,
+                                                     int64_t ld, int jacobi) {
+  extern __shared__ __align__(128) unsigned char sring[];
+  __shared__ __align__(8) uint64_t sbar[STREAM_STAGES];
+  saddle_stream<DIM>(op, nb, 1, sring, sbar, [](int) { return true; }, [&](int m) { return omegas[m]; },
+                     [&](int m) { return X + (size_t)m * ld; }, [&](int m, int row, double2 v) {
+                       if (jacobi && row < op.nfv) v = cmul(saddle_jacobi(op, row / DIM, omegas[m]), v);
+                       Y[(size_t)m * ld + row] = v;
+                     });
+}
+
 extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas_dev, const double* x_dev,
                                double* y_dev, int64_t ld, int jacobi, void* stream_) {
   if (!P || !x_dev || !y_dev || !omegas_dev || nb <= 0 || ld < P->op.n) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
   if (!P->assembled) { ss_set_error("pattern not assembled"); return SS_ERR_STATE; }
   cudaStream_t st = (cudaStream_t)stream_;
+  static int use_stream = -1;
+  if (use_stream < 0) {
+    const char* e = getenv("SS_SPMV_STREAM");
+    use_stream = e ? atoi(e) : 1;
+  }
+  if (use_stream && P->op.nchunk > 0) {
+    static bool attr = false;
+    if (!attr) {
+      SS_CUDA(cudaFuncSetAttribute((const void*)k_spmv_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, STREAM_SMEM));
+      SS_CUDA(cudaFuncSetAttribute((const void*)k_spmv_stream<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, STREAM_SMEM));
+      attr = true;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device);
+    const unsigned grid = (unsigned)std::max(1, std::min(P->op.nchunk, 2 * sms));
+    if (P->dim == 2)
+      k_spmv_stream<2><<<grid, 256, STREAM_SMEM, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
+    else
+      k_spmv_stream<3><<<grid, 256, STREAM_SMEM, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+  }
   const unsigned grid = (unsigned)saddle_nsb_host(P->nfree, P->npf);
   if (P->dim == 2)
     k_spmv_saddle<2><<<grid, 256, 0, st>>>(P->op, nb, omegas_dev, (const double2*)x_dev, (double2*)y_dev, ld, jacobi);

@@ -314,6 +314,51 @@ __device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int ph
   __syncthreads();
 }
 
+// Staged row-layout tick SpMV: true when the tick runs the persistent TMA-staged kernel.
+__host__ __device__ __forceinline__ bool tick_streamed(const KArgs& a) {
+  return a.kind == 0 && a.row_spmv && a.op.nchunk > 0;
+}
+
+// Streamed row layout (tick_streamed): persistent CTAs walk the TMA-staged chunks for the
+// INNER/START modes, then the fixed row blocks grid-stride for RESID modes (per-block partials in
+// the same fixed tree as k_tick_spmv), then one last-CTA election makes the cycle decisions.
+template <int DIM>
+__global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
+  __shared__ int sph[MAXB_SMEM];
+  __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
+  __shared__ int sflag, s_any_inner;
+  extern __shared__ __align__(128) unsigned char sring[];
+  __shared__ __align__(8) uint64_t sbar[STREAM_STAGES];
+  if (threadIdx.x == 0) s_any_inner = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.nb; b += PT) {
+    const ModeCtl* c = a.ctl + b;
+    const int ph = c->phase;
+    sph[b] = ph;
+    som[b] = c->omega;
+    sxs[b] = (ph == PH_INNER || ph == PH_START) ? a.qs[b * a.jcap + c->k] : 0.0;
+    if (ph == PH_INNER || ph == PH_START) s_any_inner = 1;
+  }
+  __syncthreads();
+  if (s_any_inner)
+    saddle_stream<DIM>(
+        a.op, a.nb, a.pstride, sring, sbar, [&](int m) { return sph[m] == PH_INNER || sph[m] == PH_START; },
+        [&](int m) { return som[m]; }, [&](int m) { return (const double2*)a.P + m; },
+        [&](int m, int row, double2 v) {
+          const double om = som[m];
+          const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
+          a.W[(size_t)m * a.ld + row] = cmul(s, cscale(v, sxs[m]));
+        });
+  for (int sb = blockIdx.x; sb < a.nsb; sb += gridDim.x)
+    for (int b = 0; b < a.nb; ++b)
+      if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
+  if (!last_cta(a, 0, 6, (int)gridDim.x, &sflag)) return;
+  for (int b = 0; b < a.nb; ++b) {
+    const int ph = sph[b];
+    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
+  }
+}
+
 // One CTA = one row block, all modes of the batch.
 template <int DIM>
 __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
@@ -373,29 +418,7 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
 // ------------------------------------------------------------------------------------------------
 enum PassKind : int { PASS_A = 1, PASS_B = 2, PASS_C = 3, PASS_X = 4 };
 
-// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+// TMA bulk-copy / mbarrier helpers: ss_spmv.cuh
 
 __device__ __forceinline__ int pass_slices(int nr) { return nr > 4 ? 1 : nr > 2 ? 2 : nr > 1 ? 4 : 8; }
 
@@ -1045,6 +1068,7 @@ struct ss_krylov {
   int64_t last_ticks = 0;
   int64_t last_launches = 0;
   double2* csr_vals_owned = nullptr;
+  int stream_ctas = 2 * 148;   // persistent CTAs of the staged tick SpMV (2 per SM)
 };
 
 template <class T>
@@ -1124,6 +1148,14 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   SS_CUDA(setattr((const void*)k_pass<PASS_B>));
   SS_CUDA(setattr((const void*)k_pass<PASS_C>));
   SS_CUDA(setattr((const void*)k_pass<PASS_X>));
+  SS_CUDA(cudaFuncSetAttribute((const void*)k_tick_spmv_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, STREAM_SMEM));
+  SS_CUDA(cudaFuncSetAttribute((const void*)k_tick_spmv_stream<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, STREAM_SMEM));
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    K->stream_ctas = 2 * sms;
+    if (const char* e = getenv("SS_STREAM_CTAS")) K->stream_ctas = std::max(1, atoi(e));
+  }
   K->ticks_per_graph = n < 200000 ? 16 : 2;
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
   K->a.x_in_a = 1;
@@ -1266,9 +1298,24 @@ extern "C" int ss_krylov_buffers(ss_krylov* K, double** rhs, double** x, int64_t
 }
 
 template <int DIM>
+static void tick_spmv_launch_dims(const ss_krylov* K, const KArgs& a, unsigned* grid, size_t* smem) {
+  if (tick_streamed(a)) {
+    *grid = (unsigned)std::max(1, std::min(a.op.nchunk, K->stream_ctas));
+    *smem = STREAM_SMEM;
+  } else {
+    *grid = (unsigned)(a.nsb * a.spmv_split);
+    *smem = 0;
+  }
+}
+
+template <int DIM>
 static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
   const unsigned gs = (unsigned)(a.nb * a.nseg);
-  k_tick_spmv<DIM><<<a.nsb * a.spmv_split, PT, 0, st>>>(a);
+  unsigned sgrid;
+  size_t ssmem;
+  tick_spmv_launch_dims<DIM>(K, a, &sgrid, &ssmem);
+  if (ssmem) k_tick_spmv_stream<DIM><<<sgrid, PT, ssmem, st>>>(a);
+  else k_tick_spmv<DIM><<<sgrid, PT, 0, st>>>(a);
   SS_LAUNCH_CHECK();
   k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
   SS_LAUNCH_CHECK();
@@ -1613,9 +1660,13 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
   for (auto& e : ev) SS_CUDA(cudaEventCreate(&e));
   int64_t tick = 0;
   int done = 0;
+  unsigned sgrid;
+  size_t ssmem;
+  tick_spmv_launch_dims<DIM>(K, a, &sgrid, &ssmem);
   while (tick < max_ticks) {
     SS_CUDA(cudaEventRecord(ev[0], st));
-    k_tick_spmv<DIM><<<a.nsb * a.spmv_split, PT, 0, st>>>(a);
+    if (ssmem) k_tick_spmv_stream<DIM><<<sgrid, PT, ssmem, st>>>(a);
+    else k_tick_spmv<DIM><<<sgrid, PT, 0, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[1], st));
     k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);

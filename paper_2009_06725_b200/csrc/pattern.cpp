@@ -36,18 +36,23 @@ extern "C" const char* ss_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t ss_launch_count(void) { return ss_launch_counter(); }
 extern "C" int ss_version(void) { return SS_ABI_VERSION; }
 
+// Device arrays carry 64 zero bytes of tail padding: the staged SpMV rounds its bulk copies to
+// 16-byte boundaries (ss_spmv.cuh stream_layout) and may read up to 15 bytes past the last entry.
+constexpr size_t SS_TAIL_PAD = 64;
+
 template <class T>
 static int upload(ss_pattern* P, const std::vector<T>& h, T** d) {
-  size_t bytes = std::max<size_t>(1, h.size()) * sizeof(T);
+  size_t bytes = std::max<size_t>(1, h.size()) * sizeof(T) + SS_TAIL_PAD;
   SS_CUDA(cudaMalloc((void**)d, bytes));
   P->allocs.push_back((void*)*d);
+  SS_CUDA(cudaMemset(*d, 0, bytes));
   if (!h.empty()) SS_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
   return SS_OK;
 }
 
 template <class T>
 static int alloc_zero(ss_pattern* P, size_t count, T** d) {
-  size_t bytes = std::max<size_t>(1, count) * sizeof(T);
+  size_t bytes = std::max<size_t>(1, count) * sizeof(T) + SS_TAIL_PAD;
   SS_CUDA(cudaMalloc((void**)d, bytes));
   P->allocs.push_back((void*)*d);
   SS_CUDA(cudaMemset(*d, 0, bytes));
@@ -245,6 +250,45 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
     P->sitems = items;
   }
 
+  // Chunks of the TMA-staged row-layout SpMV: consecutive rows while the chunk's staged matrix
+  // ranges fit one shared-memory stage (ss_spmv.cuh stream_layout), at most STREAM_VROWS node rows
+  // / STREAM_PROWS pressure rows.  A row too large for a stage disables the staged path.
+  {
+    P->crow.clear();
+    P->cent.clear();
+    bool fits = true;
+    auto vel_ent = [&](int r0, int r1) {
+      return make_int4(P->nptr[r0], P->nptr[r1], P->pptr[r0], P->pptr[r1]);
+    };
+    auto pres_ent = [&](int j0, int j1) { return make_int4(P->tptr[j0], P->tptr[j1], 0, 0); };
+    for (int r = 0; r < nfree && fits;) {
+      int r1 = r + 1;
+      if (stream_layout(vel_ent(r, r1), true, dim).bytes > STREAM_STAGE_BYTES) { fits = false; break; }
+      while (r1 < nfree && r1 - r < STREAM_VROWS &&
+             stream_layout(vel_ent(r, r1 + 1), true, dim).bytes <= STREAM_STAGE_BYTES) ++r1;
+      P->crow.push_back(make_int2(r, r1));
+      P->cent.push_back(vel_ent(r, r1));
+      r = r1;
+    }
+    const int nvchunk = (int)P->crow.size();
+    for (int j = 0; j < npf && fits;) {
+      int j1 = j + 1;
+      if (stream_layout(pres_ent(j, j1), false, dim).bytes > STREAM_STAGE_BYTES) { fits = false; break; }
+      while (j1 < npf && j1 - j < STREAM_PROWS &&
+             stream_layout(pres_ent(j, j1 + 1), false, dim).bytes <= STREAM_STAGE_BYTES) ++j1;
+      P->crow.push_back(make_int2(j, j1));
+      P->cent.push_back(pres_ent(j, j1));
+      j = j1;
+    }
+    if (!fits || (int64_t)P->pcol.size() * dim >= INT32_MAX || (int64_t)P->tcol.size() * dim >= INT32_MAX) {
+      P->crow.clear();
+      P->cent.clear();
+      P->nvchunk = 0;
+    } else {
+      P->nvchunk = nvchunk;
+    }
+  }
+
   // Constrained rows a_full[fixed_idx] (assembly.py:471-476,491): rows of fixed velocity nodes
   // (all node / vertex neighbours, global ids) and, if the pressure is pinned, the row of vertex 0.
   {
@@ -375,6 +419,15 @@ extern "C" int ss_pattern_create(int dim, int64_t n_vel_nodes, int64_t n_vertice
   UP(P->vert_pdof, vert_pdof);
   UP(P->sitems, sitems); UP(P->sbptr, sbptr);
 #undef UP
+  {
+    int2* dcrow = nullptr;
+    int4* dcent = nullptr;
+    if ((rc = upload(P, P->crow, &dcrow)) || (rc = upload(P, P->cent, &dcent))) { delete P; return rc; }
+    op.crow = dcrow;
+    op.cent = dcent;
+    op.nvchunk = P->nvchunk;
+    op.nchunk = (int)P->crow.size();
+  }
   if ((rc = upload(P, conn32, &P->d_conn))) { delete P; return rc; }
   if ((rc = upload(P, P->emap, &P->d_emap))) { delete P; return rc; }
   if ((rc = upload(P, P->color_elems, &P->d_color_elems))) { delete P; return rc; }

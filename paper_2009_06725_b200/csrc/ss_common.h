@@ -70,6 +70,10 @@ struct SsOperatorDev {
   // sbptr[b+1]) (velocity node rank r, or nfree + pressure dof), rows grouped by anchor vertex so
   // that concurrently running blocks gather from one compact window of x.
   const int* sitems; const int* sbptr;
+  // Chunks of the TMA-staged row-layout SpMV (ss_spmv.cuh saddle_stream): velocity chunks first
+  // (crow = node-rank range, cent = {nptr range, pptr range}), then pressure chunks (crow = pressure
+  // dof range, cent = {tptr range, -, -}); nchunk = 0 disables the staged path.
+  const int2* crow; const int4* cent; int nvchunk, nchunk;
 };
 
 // Generic complex CSR operator (drop-in gmres(matrix, rhs) on arbitrary matrices).

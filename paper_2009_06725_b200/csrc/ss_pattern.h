@@ -19,6 +19,9 @@ struct ss_pattern {
   // constrained rows (fixed velocity nodes; pinned pressure row)
   std::vector<int> fixed_nodes, frank, xptr, xcol, xpptr, xpcol, pincol;
   std::vector<int> sitems, sbptr;   // SpMV locality schedule (ss_common.h SsOperatorDev)
+  std::vector<int2> crow;           // staged-SpMV chunks (ss_spmv.cuh saddle_stream)
+  std::vector<int4> cent;
+  int nvchunk = 0;
   double2* d_xsm = nullptr;
   double* d_xdp = nullptr;
   double* d_pinv = nullptr;

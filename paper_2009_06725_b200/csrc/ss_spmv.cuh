@@ -30,6 +30,30 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   return make_double2((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
 }
 
+// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -320,5 +344,192 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
       }
       w[op.nfv + r] = cscale(acc, xs);
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// TMA-staged row-layout SpMV (persistent CTAs).  The matrix stream of a chunk of rows -- the
+// contiguous ncol/sm/pcol/dp ranges of up to 32 node rows, or tcol/dt of up to 32 pressure rows --
+// is moved into a shared-memory stage by bulk copies (cp.async.bulk + mbarrier, a ring of
+// STREAM_STAGES stages filled STREAM_STAGES-1 chunks ahead), so the only global loads left in the
+// compute loop are the x gathers; the staged chunk is then applied to every active mode.  The
+// per-row arithmetic is that of saddle_vel_row_g8 / saddle_pres_row (8 lanes per node row with
+// the same entry assignment and xor-shuffle tree; a warp per pressure row), so results equal the
+// row-layout saddle_block's.  Chunks (built on the host, pattern.cpp) never exceed one stage.
+// ------------------------------------------------------------------------------------------------
+constexpr int STREAM_STAGE_BYTES = 32768;
+constexpr int STREAM_STAGES = 3;
+constexpr int STREAM_SMEM = STREAM_STAGES * STREAM_STAGE_BYTES;
+constexpr int STREAM_VROWS = 32;   // node rows per velocity chunk (one 8-lane group each)
+constexpr int STREAM_PROWS = 32;   // pressure rows per chunk (one warp each, 4 per warp)
+
+struct StreamLayout {
+  int e_base, p_base, d_base;            // first staged ncol|tcol index, pcol index, dp|dt double
+  int b_col, b_sm, b_pcol, b_d;          // staged bytes of each range (multiples of 16)
+  int off_sm, off_pcol, off_d, bytes;    // stage offsets (ncol|tcol at 0)
+};
+
+__host__ __device__ __forceinline__ int ss_a16(int v) { return (v + 15) & ~15; }
+
+// ent = {e0, e1, p0, p1}: nptr/pptr ranges of a velocity chunk, or {t0, t1, -, -} (tptr) of a
+// pressure chunk.  Start indices are rounded down to 16-byte boundaries (arrays are padded at the end).
+__host__ __device__ __forceinline__ StreamLayout stream_layout(int4 ent, bool vel, int dim) {
+  StreamLayout L;
+  L.e_base = ent.x & ~3;
+  L.b_col = ss_a16((ent.y - L.e_base) * 4);
+  if (vel) {
+    L.b_sm = (ent.y - ent.x) * 16;
+    L.p_base = ent.z & ~3;
+    L.b_pcol = ss_a16((ent.w - L.p_base) * 4);
+    L.d_base = (ent.z * dim) & ~1;
+    L.b_d = ss_a16((ent.w * dim - L.d_base) * 8);
+  } else {
+    L.b_sm = 0;
+    L.p_base = 0;
+    L.b_pcol = 0;
+    L.d_base = (ent.x * dim) & ~1;
+    L.b_d = ss_a16((ent.y * dim - L.d_base) * 8);
+  }
+  L.off_sm = L.b_col;
+  L.off_pcol = L.off_sm + L.b_sm;
+  L.off_d = L.off_pcol + L.b_pcol;
+  L.bytes = L.off_d + L.b_d;
+  return L;
+}
+
+// Persistent streaming pass over all chunks for every mode m < nb with active(m):
+//   x_of(m) -> const double2* (x of mode m, element stride xs), omega_of(m), emit(m, row, value).
+template <int DIM, class Active, class Omega, class XOf, class Emit>
+__device__ __forceinline__ void saddle_stream(const SsOperatorDev& op, int nb, int xs, unsigned char* ring,
+                                              uint64_t* bar, Active active, Omega omega_of, XOf x_of, Emit emit) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  const int nmine = cta < op.nchunk ? (op.nchunk - cta + ncta - 1) / ncta : 0;
+  if (tid < STREAM_STAGES) mbar_init(&bar[tid], 1);
+  fence_mbar_init();
+  __syncthreads();
+  auto load = [&](int ci) {   // single producer thread
+    const int c = cta + ci * ncta;
+    const bool vel = c < op.nvchunk;
+    const int4 ent = op.cent[c];
+    const StreamLayout L = stream_layout(ent, vel, DIM);
+    unsigned char* st = ring + (size_t)(ci % STREAM_STAGES) * STREAM_STAGE_BYTES;
+    uint64_t* b = &bar[ci % STREAM_STAGES];
+    mbar_expect_tx(b, (unsigned)L.bytes);
+    if (vel) {
+      if (L.b_col) bulk_g2s(st, op.ncol + L.e_base, (unsigned)L.b_col, b);
+      if (L.b_sm) bulk_g2s(st + L.off_sm, op.sm + ent.x, (unsigned)L.b_sm, b);
+      if (L.b_pcol) bulk_g2s(st + L.off_pcol, op.pcol + L.p_base, (unsigned)L.b_pcol, b);
+      if (L.b_d) bulk_g2s(st + L.off_d, op.dp + L.d_base, (unsigned)L.b_d, b);
+    } else {
+      if (L.b_col) bulk_g2s(st, op.tcol + L.e_base, (unsigned)L.b_col, b);
+      if (L.b_d) bulk_g2s(st + L.off_d, op.dt + L.d_base, (unsigned)L.b_d, b);
+    }
+  };
+  if (tid == 0)
+    for (int ci = 0; ci < STREAM_STAGES - 1 && ci < nmine; ++ci) load(ci);
+  for (int ci = 0; ci < nmine; ++ci) {
+    if (tid == 0 && ci + STREAM_STAGES - 1 < nmine) load(ci + STREAM_STAGES - 1);   // stage of chunk ci-1
+    const int c = cta + ci * ncta;
+    const bool vel = c < op.nvchunk;
+    const int4 ent = __ldg(op.cent + c);
+    const int2 rows = __ldg(op.crow + c);
+    const StreamLayout L = stream_layout(ent, vel, DIM);
+    const unsigned char* st = ring + (size_t)(ci % STREAM_STAGES) * STREAM_STAGE_BYTES;
+    if (vel) {
+      const int grp = tid >> 3, gl = tid & 7;
+      const int r = rows.x + grp;
+      const bool ok = r < rows.y;
+      int e0 = 0, e1 = 0, q0 = 0, q1 = 0;
+      if (ok) {   // row ranges: global loads issued before the stage wait
+        e0 = __ldg(op.nptr + r); e1 = __ldg(op.nptr + r + 1);
+        q0 = __ldg(op.pptr + r); q1 = __ldg(op.pptr + r + 1);
+      }
+      mbar_wait(&bar[ci % STREAM_STAGES], (unsigned)((ci / STREAM_STAGES) & 1));
+      const int* scol = reinterpret_cast<const int*>(st) - L.e_base;
+      const double2* ssm = reinterpret_cast<const double2*>(st + L.off_sm) - ent.x;
+      const int* spcol = reinterpret_cast<const int*>(st + L.off_pcol) - L.p_base;
+      const double* sdp = reinterpret_cast<const double*>(st + L.off_d) - L.d_base;
+      for (int m = 0; m < nb; ++m) {
+        if (!active(m)) continue;
+        const double omega = omega_of(m);
+        const double2* __restrict__ x = x_of(m);
+        double2 acc[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
+#pragma unroll 4
+        for (int e = e0 + gl; e < e1; e += 8) {
+          const int B = scol[e];
+          const double2 a = ssm[e];
+          const double am = omega * a.y;
+          const double2* xb = x + (size_t)B * DIM * xs;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double2 v = xb[(size_t)d * xs];
+            acc[d].x += a.x * v.x - am * v.y;
+            acc[d].y += a.x * v.y + am * v.x;
+          }
+        }
+#pragma unroll 2
+        for (int e = q0 + gl; e < q1; e += 8) {
+          const double2 v = x[(size_t)(op.nfv + spcol[e]) * xs];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double dv = sdp[(size_t)e * DIM + d];
+            acc[d].x += dv * v.x;
+            acc[d].y += dv * v.y;
+          }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            acc[d].x += __shfl_xor_sync(0xffffffffu, acc[d].x, o);
+            acc[d].y += __shfl_xor_sync(0xffffffffu, acc[d].y, o);
+          }
+        if (ok && gl < DIM) {
+          double2 v = acc[0];
+#pragma unroll
+          for (int d = 1; d < DIM; ++d) if (gl == d) v = acc[d];
+          emit(m, r * DIM + gl, v);
+        }
+      }
+    } else {
+      int t0[STREAM_PROWS / 8], t1[STREAM_PROWS / 8];
+#pragma unroll
+      for (int it = 0; it < STREAM_PROWS / 8; ++it) {
+        const int j = rows.x + it * 8 + warp;
+        t0[it] = j < rows.y ? __ldg(op.tptr + j) : 0;
+        t1[it] = j < rows.y ? __ldg(op.tptr + j + 1) : 0;
+      }
+      mbar_wait(&bar[ci % STREAM_STAGES], (unsigned)((ci / STREAM_STAGES) & 1));
+      const int* scol = reinterpret_cast<const int*>(st) - L.e_base;
+      const double* sdt = reinterpret_cast<const double*>(st + L.off_d) - L.d_base;
+      for (int m = 0; m < nb; ++m) {
+        if (!active(m)) continue;
+        const double2* __restrict__ x = x_of(m);
+#pragma unroll 1
+        for (int it = 0; it < STREAM_PROWS / 8; ++it) {
+          const int j = rows.x + it * 8 + warp;
+          if (j >= rows.y) break;
+          double2 acc = make_double2(0.0, 0.0);
+          for (int e = t0[it] + lane; e < t1[it]; e += 32) {
+            const double2* xb = x + (size_t)scol[e] * DIM * xs;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) {
+              const double dv = sdt[(size_t)e * DIM + d];
+              const double2 v = xb[(size_t)d * xs];
+              acc.x += dv * v.x;
+              acc.y += dv * v.y;
+            }
+          }
+          acc.x = warp_sum(acc.x);
+          acc.y = warp_sum(acc.y);
+          if (lane == 0) emit(m, op.nfv + j, acc);
+        }
+      }
+    }
+    fence_proxy_async();   // generic-proxy reads of this stage before the async proxy refills it
+    __syncthreads();
   }
 }
