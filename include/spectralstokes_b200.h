@@ -131,13 +131,15 @@ int ss_krylov_create_csr(int device, int n, int64_t nnz, const int32_t* indptr_h
                          int max_batch, int restart, int64_t hist_cap, ss_krylov** out);
 void ss_krylov_destroy(ss_krylov* k);
 /* info[10]: n, ld, restart, n_segments, segment_rows, spmv_blocks, max_batch, ticks_per_graph,
- *           pass shared-memory bytes, kind; if info[10] == -1 on entry (12-entry buffer) also
- *           info[10] = row-layout tick SpMV, info[11] = device loop */
+ *           pass shared-memory bytes, kind */
 int ss_krylov_info(const ss_krylov* k, int64_t* info);
 /* Workspace option (drops cached graphs): "row_spmv" (0/1: mode-interleaved or row-layout tick
- * SpMV; default by n), "device_loop" (0/1), "ticks_per_graph" (1..1024).  Results never depend on
+ * SpMV; default by n), "stream_spmv" (0/1: row layout through the TMA-staged persistent kernel),
+ * "device_loop" (0/1), "ticks_per_graph" (1..1024).  Results never depend on
  * ticks_per_graph/device_loop; the SpMV layout changes no per-row summation order either. */
 int ss_krylov_set_option(ss_krylov* k, const char* name, int64_t value);
+/* Current value of a workspace option (names as for ss_krylov_set_option). */
+int ss_krylov_get_option(const ss_krylov* k, const char* name, int64_t* value);
 /* The workspace's own RHS and X buffers (nb x ld complex, device) for zero-copy callers. */
 int ss_krylov_buffers(ss_krylov* k, double** rhs_dev, double** x_dev, int64_t* ld);
 /* Solve nb modes to relative tolerance tol (krylov.py:63-164 semantics per mode).

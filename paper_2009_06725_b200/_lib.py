@@ -64,6 +64,7 @@ SIGNATURES = {
     "ss_krylov_destroy": (None, [P]),
     "ss_krylov_info": (I32, [P, PI64]),
     "ss_krylov_set_option": (I32, [P, C.c_char_p, I64]),
+    "ss_krylov_get_option": (I32, [P, C.c_char_p, PI64]),
     "ss_krylov_buffers": (I32, [P, C.POINTER(P), C.POINTER(P), PI64]),
     "ss_krylov_solve": (I32, [P, I32, PD, C.POINTER(I32), P, P, I64, I32, D, I64, I32, P, PI64, PD]),
     "ss_krylov_history": (I32, [P, I32, I64, PD]),

@@ -458,7 +458,7 @@ extern "C" int ss_spmv_batched(const ss_pattern* P, int nb, const double* omegas
   static int use_stream = -1;
   if (use_stream < 0) {
     const char* e = getenv("SS_SPMV_STREAM");
-    use_stream = e ? atoi(e) : 1;
+    use_stream = e ? atoi(e) : 0;
   }
   if (use_stream && P->op.nchunk > 0) {
     static bool attr = false;

@@ -79,6 +79,7 @@ struct KArgs {
   int gthr[3];                 // pass B: largest J using 1, 2, 4 warps per row block (8 above)
   int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
   int wide;                    // restart > WIDE_RESTART: basis passes without the shared-memory ring (any J)
+  int stream_spmv;             // row layout: TMA-staged persistent SpMV (1) or one CTA per row block (0)
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -316,7 +317,7 @@ __device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int ph
 
 // Staged row-layout tick SpMV: true when the tick runs the persistent TMA-staged kernel.
 __host__ __device__ __forceinline__ bool tick_streamed(const KArgs& a) {
-  return a.kind == 0 && a.row_spmv && a.op.nchunk > 0;
+  return a.kind == 0 && a.row_spmv && a.stream_spmv && a.op.nchunk > 0;
 }
 
 // Streamed row layout (tick_streamed): persistent CTAs walk the TMA-staged chunks for the
@@ -1155,6 +1156,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     K->stream_ctas = 2 * sms;
     if (const char* e = getenv("SS_STREAM_CTAS")) K->stream_ctas = std::max(1, atoi(e));
+    K->a.stream_spmv = 0;   // measured slower than the per-block row kernel at config 5
+    if (const char* e = getenv("SS_SPMV_STREAM")) K->a.stream_spmv = atoi(e);
   }
   K->ticks_per_graph = n < 200000 ? 16 : 2;
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
@@ -1264,6 +1267,8 @@ extern "C" int ss_krylov_set_option(ss_krylov* K, const char* name, int64_t valu
   if (opt == "row_spmv") {
     if (K->a.kind != 0 && value) { ss_set_error("row_spmv applies to the saddle operator only"); return SS_ERR_ARG; }
     K->a.row_spmv = value ? 1 : 0;
+  } else if (opt == "stream_spmv") {
+    K->a.stream_spmv = value ? 1 : 0;
   } else if (opt == "device_loop") {
     K->device_loop = value ? 1 : 0;
   } else if (opt == "ticks_per_graph") {
@@ -1279,13 +1284,23 @@ extern "C" int ss_krylov_set_option(ss_krylov* K, const char* name, int64_t valu
   return SS_OK;
 }
 
+extern "C" int ss_krylov_get_option(const ss_krylov* K, const char* name, int64_t* value) {
+  if (!K || !name || !value) { ss_set_error("null argument"); return SS_ERR_ARG; }
+  const std::string opt(name);
+  if (opt == "row_spmv") *value = K->a.row_spmv;
+  else if (opt == "stream_spmv") *value = K->a.stream_spmv;
+  else if (opt == "device_loop") *value = K->device_loop;
+  else if (opt == "ticks_per_graph") *value = K->ticks_per_graph;
+  else { ss_set_error("unknown workspace option '" + opt + "'"); return SS_ERR_ARG; }
+  return SS_OK;
+}
+
 // info: [n, ld, restart, nseg, seg_rows, nsb, max_batch, ticks_per_graph, smem_pass, kind]
 extern "C" int ss_krylov_info(const ss_krylov* K, int64_t* info) {
   if (!K || !info) { ss_set_error("null argument"); return SS_ERR_ARG; }
   info[0] = K->a.n; info[1] = K->a.ld; info[2] = K->a.restart; info[3] = K->a.nseg; info[4] = K->a.seg_rows;
   info[5] = K->a.nsb; info[6] = K->max_batch; info[7] = K->ticks_per_graph; info[8] = (int64_t)K->smem_pass;
   info[9] = K->a.kind;
-  if (info[10] == -1) { info[10] = K->a.row_spmv; info[11] = K->device_loop; }
   return SS_OK;
 }
 

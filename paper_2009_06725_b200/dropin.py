@@ -28,10 +28,10 @@ import importlib
 import importlib.util
 import sys
 
-from . import _lib, assembly, errors, io, krylov, mesh, metrics, spectral, structured, vessels
+from . import _lib, assembly, boundary, errors, io, krylov, mesh, metrics, spectral, structured, vessels
 
 NAME = "spectralstokes"
-_OURS = [sys.modules[__package__], _lib, assembly, errors, io, krylov, mesh, metrics, spectral, structured, vessels]
+_OURS = [sys.modules[__package__], _lib, assembly, boundary, errors, io, krylov, mesh, metrics, spectral, structured, vessels]
 _SUBMODULES = {"assembly": assembly, "krylov": krylov, "spectral": spectral, "mesh": mesh, "errors": errors,
                "metrics": metrics, "structured": structured, "io": io}
 

@@ -84,10 +84,12 @@ class KrylovWorkspace:
         _lib.call("ss_krylov_set_option", self._h, name.encode(), int(value))
 
     def options(self):
-        info = np.zeros(12, dtype=np.int64)
-        info[10] = -1
-        _lib.call("ss_krylov_info", self._h, _lib.ptr(info, C.c_int64))
-        return {"row_spmv": int(info[10]), "device_loop": int(info[11]), "ticks_per_graph": int(info[7])}
+        out = {}
+        for name in ("row_spmv", "stream_spmv", "device_loop", "ticks_per_graph"):
+            v = C.c_int64()
+            _lib.call("ss_krylov_get_option", self._h, name.encode(), C.byref(v))
+            out[name] = int(v.value)
+        return out
 
     @classmethod
     def for_operator(cls, op, restart: int, max_batch: int, hist_cap: int):

@@ -1,7 +1,8 @@
 """GPU parity of the layout-dependent engine paths that the default test configs do not reach.
 
 * The row-layout tick SpMV (8 lanes per node row reading one mode's strided column of P) is what
-  every solve with n >= 25 M DOFs runs -- i.e. all of BASELINE config 5.  It is forced here on the
+  every solve with n >= 25 M DOFs runs -- i.e. all of BASELINE config 5 -- in both variants: one
+  CTA per row block, and the TMA-staged persistent kernel (``stream_spmv``).  It is forced here on the
   small instances (``ss_krylov_set_option(k, "row_spmv", 1)``) and checked against the reference:
   fixed-budget history and iterate (c1, tests/golden/c1.npz) and converged fields at 1e-10
   (pipe3d, the config-5 generator's small instance; tests/golden/pipe3d.npz, small3d.npz).
@@ -63,8 +64,9 @@ def test_row_layout_fixed_budget_matches_reference():
     np.testing.assert_allclose(rep2.residual_history, rep.residual_history, rtol=1e-9)
 
 
+@pytest.mark.parametrize("staged", [0, 1])
 @pytest.mark.parametrize("which", ["pipe3d", "c5_small"])
-def test_row_layout_converged_fields_match_reference(which):
+def test_row_layout_converged_fields_match_reference(which, staged):
     if which == "pipe3d":
         case, g, idx = pipe3d_case(), golden("pipe3d.npz"), [1, 16]
         key = lambda i, f: f"{f}_{i}"  # noqa: E731
@@ -74,7 +76,8 @@ def test_row_layout_converged_fields_match_reference(which):
     props = FluidProps(case.density, case.viscosity)
     op = get_operator(case.qmesh, props)
     settings = SolverSettings(tolerance=C1_TOL, restart=200)
-    with workspace_option(op, 200, len(idx), settings.max_iterations, "row_spmv", 1):
+    with workspace_option(op, 200, len(idx), settings.max_iterations, "row_spmv", 1), \
+            workspace_option(op, 200, len(idx), settings.max_iterations, "stream_spmv", staged):
         sols = solve_mode_systems(case.qmesh, props, idx, case.omegas[idx],
                                   [case.coefficients[i] * case.profile for i in idx], None, settings)
     for s in sols:
