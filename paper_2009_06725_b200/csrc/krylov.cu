@@ -360,8 +360,10 @@ __global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
   }
 }
 
-// One CTA = one row block, all modes of the batch.
-template <int DIM>
+// One CTA = one row block, all modes of the batch.  ROW: the row-layout INNER SpMV (8 lanes per
+// node row, the mode's strided column of P), instantiated separately so its register allocation is
+// not shaped by the mode-interleaved kernel.
+template <int DIM, int ROW>
 __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   __shared__ int sph[MAXB_SMEM];
   __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
@@ -378,29 +380,35 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
     if (ph == PH_INNER || ph == PH_START) s_any_inner = 1;
   }
   __syncthreads();
-  if (s_any_inner) {
-    if (a.kind == 0 && a.row_spmv) {
-      // very large n (rule on n only, so per-mode results stay batch-invariant; at most a few modes
-      // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
-      // the mode's column of P with stride pstride (1.7x the interleaved kernel at one mode)
-      for (int b = sub; b < a.nb; b += a.spmv_split) {
-        if (sph[b] != PH_INNER && sph[b] != PH_START) continue;
-        const double om = som[b], xs = sxs[b];
-        double2* w = a.W + (size_t)b * a.ld;
-        saddle_block<DIM>(a.op, sb, om, a.P + b, [&](int row, double2 v) {
-          const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
-          w[row] = cmul(s, cscale(v, xs));
-        }, a.pstride);
-      }
-    } else if (a.kind == 0) {
-      spmv_inner_interleaved<DIM>(a, sb, sph, som, sxs);
+  if (ROW) {
+    // very large n (rule on n only, so per-mode results stay batch-invariant; at most a few modes
+    // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
+    // the mode's column of P with stride pstride.  Grid-stride over the row blocks (a few CTAs per
+    // SM): the mode-state prologue and the last-CTA election are paid per CTA, not per block.
+    for (int blk = blockIdx.x; blk < a.nsb; blk += gridDim.x) {
+      if (s_any_inner)
+        for (int b = 0; b < a.nb; ++b) {
+          if (sph[b] != PH_INNER && sph[b] != PH_START) continue;
+          const double om = som[b], xs = sxs[b];
+          double2* w = a.W + (size_t)b * a.ld;
+          saddle_block<DIM>(a.op, blk, om, a.P + b, [&](int row, double2 v) {
+            const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
+            w[row] = cmul(s, cscale(v, xs));
+          }, a.pstride);
+        }
+      for (int b = 0; b < a.nb; ++b)
+        if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, blk, som[b]);
+    }
+  } else if (s_any_inner) {
+    if (a.kind == 0) {
+      if (!ROW) spmv_inner_interleaved<DIM>(a, sb, sph, som, sxs);
     } else {
       if (sub == 0)
         for (int b = 0; b < a.nb; ++b)
           if (sph[b] == PH_INNER || sph[b] == PH_START) spmv_inner_csr_mode(a, b, sb, sxs[b]);
     }
   }
-  if (sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
+  if (!ROW && sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
     for (int b = 0; b < a.nb; ++b)
       if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
   // one election for the whole batch (slot 6 of mode 0's counters): the last CTA to finish makes
@@ -1070,6 +1078,7 @@ struct ss_krylov {
   int64_t last_launches = 0;
   double2* csr_vals_owned = nullptr;
   int stream_ctas = 2 * 148;   // persistent CTAs of the staged tick SpMV (2 per SM)
+  int row_ctas = 16 * 148;     // grid-stride CTAs of the row-layout tick SpMV
 };
 
 template <class T>
@@ -1155,6 +1164,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     K->stream_ctas = 2 * sms;
+    K->row_ctas = 16 * sms;
+    if (const char* e = getenv("SS_ROW_CTAS")) K->row_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("SS_STREAM_CTAS")) K->stream_ctas = std::max(1, atoi(e));
     K->a.stream_spmv = 0;   // measured slower than the per-block row kernel at config 5
     if (const char* e = getenv("SS_SPMV_STREAM")) K->a.stream_spmv = atoi(e);
@@ -1317,6 +1328,9 @@ static void tick_spmv_launch_dims(const ss_krylov* K, const KArgs& a, unsigned* 
   if (tick_streamed(a)) {
     *grid = (unsigned)std::max(1, std::min(a.op.nchunk, K->stream_ctas));
     *smem = STREAM_SMEM;
+  } else if (a.kind == 0 && a.row_spmv) {
+    *grid = (unsigned)std::max(1, std::min(a.nsb, K->row_ctas));
+    *smem = 0;
   } else {
     *grid = (unsigned)(a.nsb * a.spmv_split);
     *smem = 0;
@@ -1330,7 +1344,8 @@ static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
   size_t ssmem;
   tick_spmv_launch_dims<DIM>(K, a, &sgrid, &ssmem);
   if (ssmem) k_tick_spmv_stream<DIM><<<sgrid, PT, ssmem, st>>>(a);
-  else k_tick_spmv<DIM><<<sgrid, PT, 0, st>>>(a);
+  else if (a.kind == 0 && a.row_spmv) k_tick_spmv<DIM, 1><<<sgrid, PT, 0, st>>>(a);
+  else k_tick_spmv<DIM, 0><<<sgrid, PT, 0, st>>>(a);
   SS_LAUNCH_CHECK();
   k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
   SS_LAUNCH_CHECK();
@@ -1681,7 +1696,8 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
   while (tick < max_ticks) {
     SS_CUDA(cudaEventRecord(ev[0], st));
     if (ssmem) k_tick_spmv_stream<DIM><<<sgrid, PT, ssmem, st>>>(a);
-    else k_tick_spmv<DIM><<<sgrid, PT, 0, st>>>(a);
+    else if (a.kind == 0 && a.row_spmv) k_tick_spmv<DIM, 1><<<sgrid, PT, 0, st>>>(a);
+    else k_tick_spmv<DIM, 0><<<sgrid, PT, 0, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[1], st));
     k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);

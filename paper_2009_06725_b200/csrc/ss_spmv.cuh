@@ -60,6 +60,39 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Matrix-stream loads of the row-layout SpMV.  SS_MATRIX_LOAD_NA=1 streams the (read-once) matrix
+// with ld.global.nc.L1::no_allocate so L1 keeps the x-gather lines; 0 = plain __ldg.
+#ifndef SS_MATRIX_LOAD_NA
+#define SS_MATRIX_LOAD_NA 0
+#endif
+__device__ __forceinline__ int ldm(const int* p) {
+#if SS_MATRIX_LOAD_NA
+  int v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ldm(const double* p) {
+#if SS_MATRIX_LOAD_NA
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 ldm(const double2* p) {
+#if SS_MATRIX_LOAD_NA
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // Jacobi scale of velocity node row r at frequency w: 1/(S'_rr + i w M'_rr), 1 if that is 0
 // (krylov.py:49-60 on the reduced matrix's diagonal; the pressure diagonal is 0 -> 1).
 __device__ __forceinline__ double2 saddle_jacobi(const SsOperatorDev& op, int r, double omega) {
@@ -114,10 +147,10 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
   double2 acc = make_double2(0.0, 0.0);
   const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
   for (int e = e0 + lane; e < e1; e += 32) {
-    const double2* xb = x + (size_t)__ldg(op.tcol + e) * DIM * xs;
+    const double2* xb = x + (size_t)ldm(op.tcol + e) * DIM * xs;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-      const double dv = __ldg(op.dt + (size_t)e * DIM + d);
+      const double dv = ldm(op.dt + (size_t)e * DIM + d);
       const double2 v = xb[(size_t)d * xs];
       acc.x += dv * v.x;
       acc.y += dv * v.y;
@@ -171,8 +204,8 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
 #pragma unroll 4
     for (int e = e0 + gl; e < e1; e += 8) {
-      const int B = __ldg(op.ncol + e);
-      const double2 a = __ldg(op.sm + e);
+      const int B = ldm(op.ncol + e);
+      const double2 a = ldm(op.sm + e);
       const double am = omega * a.y;
       const double2* xb = x + (size_t)B * DIM * xs;
 #pragma unroll
@@ -185,10 +218,10 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
 #pragma unroll 2
     for (int e = p0 + gl; e < p1; e += 8) {
-      const double2 v = x[(size_t)(op.nfv + __ldg(op.pcol + e)) * xs];
+      const double2 v = x[(size_t)(op.nfv + ldm(op.pcol + e)) * xs];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        const double dv = __ldg(op.dp + (size_t)e * DIM + d);
+        const double dv = ldm(op.dp + (size_t)e * DIM + d);
         acc[d].x += dv * v.x;
         acc[d].y += dv * v.y;
       }

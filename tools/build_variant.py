@@ -1,7 +1,8 @@
 """Build the native library from another revision's csrc (A/B timing): variants/<name>.so.
 
 usage: python tools/build_variant.py <git-rev | .> <name> [-DMACRO ...]   ('.' = working tree)
-Load it with SS_B200_LIB=variants/<name>.so (one variant per process).
+Load it with SS_B200_LIB=tools/_variants/<name>.so (one variant per process; the directory travels
+with gpurun snapshots, the .so files stay out of git).
 """
 import subprocess
 import sys
@@ -15,7 +16,7 @@ from paper_2009_06725_b200 import build as B  # noqa: E402
 rev, name, defines = sys.argv[1], sys.argv[2], sys.argv[3:]
 overrides = dict(d[len("--src="):].split("=", 1) for d in defines if d.startswith("--src="))   # --src=krylov.cu=/path
 defines = [d for d in defines if not d.startswith("--src=")]
-out = ROOT / "variants"
+out = ROOT / "tools" / "_variants"
 out.mkdir(exist_ok=True)
 with tempfile.TemporaryDirectory() as td:
     td = Path(td)
@@ -38,5 +39,5 @@ with tempfile.TemporaryDirectory() as td:
         (out / f"{name}.{src}.ptxas.log").write_text(r.stderr)
         objs.append(str(obj))
     subprocess.run([B._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fopenmp",
-                    *objs, "-o", str(out / f"{name}.so"), "-lcudart", "-lgomp"], check=True)
+                    *objs, "-o", str(out / f"{name}.so"), "-lcudart", "-lgomp", "-ldl"], check=True)
 print(out / f"{name}.so")
