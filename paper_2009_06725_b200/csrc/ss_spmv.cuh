@@ -93,33 +93,6 @@ __device__ __forceinline__ double2 ldm(const double2* p) {
 #endif
 }
 
-// All DIM complex components of node B from a contiguous x (stride 1) with 256-bit loads
-// (LDG.E.ENL2.256): the node's DIM*16 bytes lie in two (3D) or one (2D) 32-byte-aligned pieces, so
-// a gather costs 2 (1) L1 requests instead of DIM.  x must be 32-byte aligned and readable one
-// element past node B's last component (true for every reduced vector: pressures follow the
-// velocity block and ld >= n is padded).
-__device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
-  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
-}
-template <int DIM>
-__device__ __forceinline__ void ld_node(const double2* __restrict__ x, int B, double2 (&v)[DIM]) {
-  if constexpr (DIM == 3) {
-    const int odd = B & 1;
-    const double* a0 = reinterpret_cast<const double*>(x + (size_t)3 * B - odd);
-    double r0, r1, r2, r3, r4, r5, r6, r7;
-    ld256(a0, r0, r1, r2, r3);
-    ld256(a0 + 4, r4, r5, r6, r7);
-    v[0] = odd ? make_double2(r2, r3) : make_double2(r0, r1);
-    v[1] = odd ? make_double2(r4, r5) : make_double2(r2, r3);
-    v[2] = odd ? make_double2(r6, r7) : make_double2(r4, r5);
-  } else {
-    double r0, r1, r2, r3;
-    ld256(reinterpret_cast<const double*>(x + (size_t)2 * B), r0, r1, r2, r3);
-    v[0] = make_double2(r0, r1);
-    v[1] = make_double2(r2, r3);
-  }
-}
-
 // Jacobi scale of velocity node row r at frequency w: 1/(S'_rr + i w M'_rr), 1 if that is 0
 // (krylov.py:49-60 on the reduced matrix's diagonal; the pressure diagonal is 0 -> 1).
 __device__ __forceinline__ double2 saddle_jacobi(const SsOperatorDev& op, int r, double omega) {
@@ -173,27 +146,14 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
                                                    const double2* __restrict__ x, int lane, int xs = 1) {
   double2 acc = make_double2(0.0, 0.0);
   const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
-  if (xs == 1) {
-    for (int e = e0 + lane; e < e1; e += 32) {
-      double2 v[DIM];
-      ld_node<DIM>(x, ldm(op.tcol + e), v);
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const double2* xb = x + (size_t)ldm(op.tcol + e) * DIM * xs;
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const double dv = ldm(op.dt + (size_t)e * DIM + d);
-        acc.x += dv * v[d].x;
-        acc.y += dv * v[d].y;
-      }
-    }
-  } else {
-    for (int e = e0 + lane; e < e1; e += 32) {
-      const double2* xb = x + (size_t)ldm(op.tcol + e) * DIM * xs;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const double dv = ldm(op.dt + (size_t)e * DIM + d);
-        const double2 v = xb[(size_t)d * xs];
-        acc.x += dv * v.x;
-        acc.y += dv * v.y;
-      }
+    for (int d = 0; d < DIM; ++d) {
+      const double dv = ldm(op.dt + (size_t)e * DIM + d);
+      const double2 v = xb[(size_t)d * xs];
+      acc.x += dv * v.x;
+      acc.y += dv * v.y;
     }
   }
   acc.x = warp_sum(acc.x);
@@ -242,33 +202,17 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
   if (r >= 0) {
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-    if (xs == 1) {
 #pragma unroll 4
-      for (int e = e0 + gl; e < e1; e += 8) {
-        const int B = ldm(op.ncol + e);
-        const double2 a = ldm(op.sm + e);
-        const double am = omega * a.y;
-        double2 v[DIM];
-        ld_node<DIM>(x, B, v);
+    for (int e = e0 + gl; e < e1; e += 8) {
+      const int B = ldm(op.ncol + e);
+      const double2 a = ldm(op.sm + e);
+      const double am = omega * a.y;
+      const double2* xb = x + (size_t)B * DIM * xs;
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          acc[d].x += a.x * v[d].x - am * v[d].y;
-          acc[d].y += a.x * v[d].y + am * v[d].x;
-        }
-      }
-    } else {
-#pragma unroll 4
-      for (int e = e0 + gl; e < e1; e += 8) {
-        const int B = ldm(op.ncol + e);
-        const double2 a = ldm(op.sm + e);
-        const double am = omega * a.y;
-        const double2* xb = x + (size_t)B * DIM * xs;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          const double2 v = xb[(size_t)d * xs];
-          acc[d].x += a.x * v.x - am * v.y;
-          acc[d].y += a.x * v.y + am * v.x;
-        }
+      for (int d = 0; d < DIM; ++d) {
+        const double2 v = xb[(size_t)d * xs];
+        acc[d].x += a.x * v.x - am * v.y;
+        acc[d].y += a.x * v.y + am * v.x;
       }
     }
     const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
