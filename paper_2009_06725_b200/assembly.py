@@ -365,12 +365,26 @@ class SaddleOperator:
                 ws.close()
             self._krylov.clear()
 
-    def max_batch(self, restart: int) -> int:
-        """Modes that fit one GPU at this restart (basis is (restart+1)*ld*16 B per mode)."""
+    def workspace_bytes(self, restart: int, nb: int, hist_cap: int) -> int:
+        """Device bytes of a Krylov workspace for ``nb`` modes (mirrors krylov_common_init and
+        ss_krylov_create_saddle: basis, W/P/X/RHS, Hessenberg, Givens, partials, history)."""
+        ld = self.ld
+        jcap = restart + 1
+        seg = min(6144, max(256, ((ld + 15) // 16 + 31) // 32 * 32))   # krylov_common_init segment rows
+        nseg = -(-ld // seg)
+        nsb = -(-self.n_free_nodes // 128) + -(-self.n_free_pressures // 32)
+        per_mode = 16 * (jcap * ld + 4 * ld + restart * jcap + 4 * jcap + 2 * restart + nseg * jcap + nsb) \
+            + 8 * (jcap + max(1, hist_cap)) + 32 + 96
+        return nb * per_mode + 4096
+
+    def max_batch(self, restart: int, hist_cap: int = 200_000) -> int:
+        """Modes whose Krylov workspaces fit this GPU now: free HBM minus a reserve (1 GiB + 2 % of
+        the device), divided by the exact per-mode workspace size."""
         torch = _lib.torch_mod()
-        free, _ = torch.cuda.mem_get_info(self.device)
-        per_mode = (restart + 1 + 8) * self.ld * 16 + (restart + 1) * restart * 16
-        return max(1, min(256, int(0.85 * free // per_mode)))   # 256: krylov.MAX_BATCH
+        free, total = torch.cuda.mem_get_info(self.device)
+        reserve = (1 << 30) + total // 50
+        per_mode = self.workspace_bytes(restart, 1, hist_cap)
+        return max(1, min(256, int((free - reserve) // per_mode)))   # 256: krylov.MAX_BATCH
 
 
 _OP_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()

@@ -115,3 +115,30 @@ def test_config5_full_size():
     case = c5_case()
     assert case.mesh.n_elements > 7_900_000
     _full_size_checks(case, [1], restart=30, budget=40)
+
+
+@pytest.mark.parametrize("make,expect", [(c3_case, 5), (c4_case, 2), (c5_case, 1)])
+def test_full_size_batches_fit_hbm(make, expect):
+    """HBM planning: max_batch at restart 200 is the configs' expected batch (c3 ~ 6,
+    c4 ~ 2, c5 ~ 1), the workspace of that size allocates, and its measured footprint matches
+    SaddleOperator.workspace_bytes within 1 %."""
+    case = make()
+    props = FluidProps(case.density, case.viscosity)
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    op = get_operator(case.qmesh, props)
+    op.release_workspaces()
+    torch.cuda.synchronize()
+    nb = op.max_batch(200, 200)
+    assert expect <= nb <= expect + 1
+    free0, _ = torch.cuda.mem_get_info()
+    ws = op.krylov(200, nb, 200)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    used = free0 - free1
+    want = op.workspace_bytes(200, nb, 200)
+    assert abs(used - want) <= 0.01 * want + (64 << 20), (used, want)
+    assert ws.max_batch == nb
+    op.release_workspaces()
