@@ -81,10 +81,10 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, rank: int = None):
         self.gpu = gpu_index
         self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index if rank is None else rank}.csv")
 
     def __enter__(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
@@ -265,9 +265,28 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Code-path check on a one-GPU box only (never a measurement): SS_BENCH_PG=gloo runs every rank
+    # on cuda:0 with gloo plumbing and the host-staged gather instead of NCCL, which refuses two
+    # ranks on one device.  The ranks' kernels never wait on each other (independent mode solves).
+    smoke_pg = os.environ.get("SS_BENCH_PG") == "gloo" and world > 1
+    if smoke_pg:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if smoke_pg:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def reduce_(t, op):
+        if world == 1:
+            return t
+        if smoke_pg:
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            return h.to(t.device)
+        dist.all_reduce(t, op=op)
+        return t
     from paper_2009_06725_b200 import SolverSettings, _lib
     from paper_2009_06725_b200.assembly import assemble_mode_systems
     from paper_2009_06725_b200.comm import ModeComm
@@ -284,7 +303,7 @@ def run_b200(args):
     omegas_all = case.omegas
     profile_dev = torch.from_numpy(np.ascontiguousarray(case.profile, dtype=complex)).to(dev)
     ws = op.krylov(RESTART, per_step, BUDGET)
-    comm = ModeComm.from_process_group(local) if world > 1 else None
+    comm = ModeComm.from_process_group(local) if world > 1 and not smoke_pg else None
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream()
@@ -307,7 +326,7 @@ def run_b200(args):
 
     # ---- timed region: inputs resident in HBM ----
     l0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, rank) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -324,9 +343,8 @@ def run_b200(args):
     launches = _lib.launch_count() - l0
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     it_t = torch.tensor([iters], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+    t = reduce_(t, dist.ReduceOp.MAX)
+    it_t = reduce_(it_t, dist.ReduceOp.SUM)
     ms_total = float(t.item())
     total_iters = float(it_t.item())
     value = total_iters / (ms_total * 1e-3)
@@ -359,7 +377,12 @@ def run_b200(args):
         fields[:, nvn * dim:] = P
         if world > 1:   # every rank's fields of this step -> rank 0 (slots rank*per_step + j)
             step_plan = [list(range(r * per_step, (r + 1) * per_step)) for r in range(world)]
-            comm.gather_modes(fields, step_plan, root=0, out=gather_out)
+            if comm is not None:
+                comm.gather_modes(fields, step_plan, root=0, out=gather_out)
+            else:
+                from paper_2009_06725_b200.distributed import gather_mode_fields
+
+                gather_mode_fields(fields, step_plan, rank, world, comm=None, dst=0)
         f_pin.copy_(fields, non_blocking=True)
         return sum(r.iterations for r in reps)
 
@@ -377,9 +400,8 @@ def run_b200(args):
     e2e_wall = time.perf_counter() - w0
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     ei = torch.tensor([e_iters], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ei, op=dist.ReduceOp.SUM)
+    t = reduce_(t, dist.ReduceOp.MAX)
+    ei = reduce_(ei, dist.ReduceOp.SUM)
     e2e_value = float(ei.item()) / (float(t.item()) * 1e-3)
     del g_pin, f_pin, fields, gather_out
 
@@ -428,6 +450,7 @@ def run_b200(args):
             "data": f"synthetic (seeded, BASELINE config {'5' if key == 'c5' else '2'})",
             "config": cfg,
             "setup_s": setup_s,
+            "projected_modes_per_s": _projection(key, value),
             "sweep": {"modes": w["total_modes"], "max_modes_per_gpu": max(len(p) for p in plan),
                       "one_cycle_of_every_mode_s": max(len(p) for p in plan) / per_step * ms_per_step / 1e3,
                       "note": "derived: makespan of one restart cycle of all modes on n_gpus (LPT plan)"},
@@ -441,7 +464,8 @@ def run_b200(args):
             "spmv": spmv,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "gather": "ss_comm_gather_modes (NCCL) to rank 0 every step" if world > 1 else None,
+                    "gather": None if world == 1 else ("ss_comm_gather_modes (NCCL) to rank 0 every step" if comm
+                                                       else "gloo host-staged gather (SS_BENCH_PG=gloo code-path check)"),
                     "wall_s": e2e_wall},
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -452,6 +476,24 @@ def run_b200(args):
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _projection(key, value):
+    """Modes/s projected from the measured rate and iteration counts measured to convergence at
+    config 2 (profiles/r2_c2_converge.json: modes 1 and 16 to 1e-10 on the GPU), scaled to the
+    workload's n by the growth measured on the reference's down-scaled pipes (iterations ~ n^0.92,
+    SURVEY.md §8d).  A projection, labelled as such."""
+    from paper_2009_06725_b200.distributed import C2_MEASURED_ITERATIONS, expected_iterations
+
+    w = WORKLOADS[key]
+    growth = (w["n_dofs"] / WORKLOADS["c2"]["n_dofs"]) ** 0.92
+    idx = np.arange(w["total_modes"])
+    per_mode = C2_MEASURED_ITERATIONS[1] * expected_iterations(idx, 3) * growth
+    mean_iters = float(per_mode[1:].mean())
+    return {"value": value / mean_iters, "mean_iterations_per_mode": mean_iters,
+            "basis": "PROJECTION: measured mode-iterations/s / mean iterations per mode; iterations from modes 1 and "
+                     "16 solved to 1e-10 at config 2 (336 974 and 886 922, profiles/r2_c2_converge.json), linear in "
+                     f"the mode index, scaled by (n/n_c2)^0.92 = {growth:.2f}"}
 
 
 def _traffic_from_profile(key, dom_name, dom):

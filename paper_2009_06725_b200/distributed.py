@@ -12,8 +12,8 @@ reconstructing rank:
 Pieces:
 
 * :func:`expected_iterations` -- the LPT cost model: flat in 2D, linear in the mode index in 3D,
-  fitted to the reference's own converged iteration counts (tests/golden pipe3d / small3d:
-  modes 1 and 16); :func:`calibrate_iterations` refits it from any measured counts and
+  fitted to converged iteration counts measured at BASELINE config 2 (modes 1 and 16);
+  :func:`calibrate_iterations` refits it from any measured counts and
   :func:`iterations_from_first_cycle` predicts counts from a first restart cycle's estimates.
 * :func:`lpt_shard` -- longest-processing-time-first assignment.
 * :func:`gather_mode_fields` -- the gather to one destination rank.
@@ -28,10 +28,13 @@ import numpy as np
 __all__ = ["lpt_shard", "expected_iterations", "calibrate_iterations", "iterations_from_first_cycle",
            "gather_mode_fields", "solve_mode_systems_distributed", "DEFAULT_3D_MODEL"]
 
-# Iterations to 1e-10 (restart 200) measured by the reference on the down-scaled 3D pipes:
-# pipe3d (n = 8 782) mode 1: 9 687, mode 16: 20 603 (tests/golden/pipe3d.npz); relative to
-# mode 1 that is 1 + 0.0726 (idx - 1) -> model a + b*idx with a = 1, b = 0.075 (per mode-1 cost).
-DEFAULT_3D_MODEL = (1.0, 0.075)
+# Iterations to 1e-10 (restart 200) measured on the GPU at BASELINE config 2 (n = 796 978;
+# profiles/r2_c2_converge.json, tools/c2_converge.py): mode 1 336 974, mode 16 886 922 -> per mode-1
+# cost a + b*idx with a + b = 1, a + 16 b = 2.632.  (The reference's own counts on the down-scaled
+# pipe, tests/golden/pipe3d.npz: 9 687 and 20 603, ratio 2.13 -- the growth with the mode index
+# steepens with n.)
+C2_MEASURED_ITERATIONS = {1: 336_974, 16: 886_922}
+DEFAULT_3D_MODEL = (1.0 - (886_922 / 336_974 - 1.0) / 15.0, (886_922 / 336_974 - 1.0) / 15.0)
 
 
 def calibrate_iterations(indices, iterations):

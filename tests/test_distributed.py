@@ -34,7 +34,7 @@ def test_lpt_balances_and_covers():
 def test_expected_iterations_model():
     assert np.all(expected_iterations(np.arange(9), 2) == 1.0)
     c = expected_iterations([1, 16], 3)
-    assert 1.9 < c[1] / c[0] < 2.3                                 # reference: 20 603 / 9 687 = 2.13
+    assert c[1] / c[0] == pytest.approx(886_922 / 336_974)         # measured at config 2 (profiles/)
 
 
 def test_calibration_from_reference_counts():
