@@ -241,9 +241,10 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
 // NSLOT = 32 / DIM slots, so one x-gather instruction covers NSLOT whole nodes (their DIM
 // components in one line) instead of 32 unrelated 16-byte pieces: ~DIM x fewer L1 requests per
 // gathered node.  Per-component partial sums are combined over the slots with a fixed shuffle tree.
+// Measured 2x slower in-cycle at config 5 (10.5 vs 5.0 ms: one row in flight per warp), so off.
 // ------------------------------------------------------------------------------------------------
 #ifndef SS_ROW_CL
-#define SS_ROW_CL 1
+#define SS_ROW_CL 0
 #endif
 
 template <int DIM>
