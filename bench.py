@@ -420,8 +420,13 @@ def run_b200(args):
 
     # ---- the tick SpMV standalone (second half of the metric) ----
     spmv = _spmv_numbers(op, omegas_all[ms0], ws, e0, e1, stream, hbm_peak, torch)
-    spmv["share_of_cycle"] = prof["spmv"]["ms"] / total_ms
-    spmv["in_cycle_gbs"] = (op.spmv_bytes(per_step) * prof["spmv"]["launches"]) / (prof["spmv"]["ms"] * 1e-3) / 1e9
+    # headline SpMV figure: the tick's SpMV inside the instrumented cycle (CUDA events around each
+    # launch on the solve stream); the standalone call is kept beside it
+    in_cycle_ms = prof["spmv"]["ms"] / max(1, prof["spmv"]["launches"])
+    in_gbs = op.spmv_bytes(per_step) / (in_cycle_ms * 1e-3) / 1e9
+    spmv.update({"standalone_ms": spmv["ms"], "standalone_gbs": spmv["achieved_gbs"], "ms": in_cycle_ms,
+                 "achieved_gbs": in_gbs, "frac": in_gbs / hbm_peak, "share_of_cycle": prof["spmv"]["ms"] / total_ms,
+                 "measured": "in-cycle (instrumented cycle, per launch); standalone_* = one isolated call"})
 
     extras = {}
     if rank == 0 and world == 1 and not args.quick:
