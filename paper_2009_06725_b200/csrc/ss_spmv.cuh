@@ -194,6 +194,12 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
   return (nfree + SPMV_VROWS - 1) / SPMV_VROWS + (npf + SPMV_PROWS - 1) / SPMV_PROWS;
 }
 
+// Lanes per node row of the row-layout SpMV (8: four rows per warp; 16: two).
+#ifndef SS_ROW_LANES
+#define SS_ROW_LANES 8
+#endif
+constexpr int ROW_LANES = SS_ROW_LANES;
+
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
                                                   const double2* __restrict__ x, int gl, double2 (&acc)[DIM],
@@ -203,7 +209,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
   if (r >= 0) {
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
 #pragma unroll 4
-    for (int e = e0 + gl; e < e1; e += 8) {
+    for (int e = e0 + gl; e < e1; e += ROW_LANES) {
       const int B = ldm(op.ncol + e);
       const double2 a = ldm(op.sm + e);
       const double am = omega * a.y;
@@ -217,7 +223,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     }
     const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
 #pragma unroll 2
-    for (int e = p0 + gl; e < p1; e += 8) {
+    for (int e = p0 + gl; e < p1; e += ROW_LANES) {
       const double2 v = x[(size_t)(op.nfv + ldm(op.pcol + e)) * xs];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
@@ -228,7 +234,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     }
   }
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1)
+  for (int o = ROW_LANES / 2; o > 0; o >>= 1)
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       acc[d].x += __shfl_xor_sync(0xffffffffu, acc[d].x, o);
@@ -340,10 +346,11 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
   return;
 #endif
   if (blk < nvb) {
-    const int grp = lane >> 3, gl = lane & 7;
+    constexpr int RPW = 32 / ROW_LANES;   // rows per warp per iteration
+    const int grp = lane / ROW_LANES, gl = lane % ROW_LANES;
 #pragma unroll 1
-    for (int it = 0; it < SPMV_VROWS / 32; ++it) {
-      const int r = blk * SPMV_VROWS + it * 32 + warp * 4 + grp;
+    for (int it = 0; it < SPMV_VROWS / (8 * RPW); ++it) {
+      const int r = blk * SPMV_VROWS + it * 8 * RPW + warp * RPW + grp;
       const bool ok = r < op.nfree;
       double2 acc[DIM];
       saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc, xs);
