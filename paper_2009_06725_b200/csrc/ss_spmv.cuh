@@ -242,109 +242,12 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
     }
 }
 
-// ------------------------------------------------------------------------------------------------
-// Component-lane row mapping (SS_ROW_CL): a warp per row, lane = (entry slot, component d) with
-// NSLOT = 32 / DIM slots, so one x-gather instruction covers NSLOT whole nodes (their DIM
-// components in one line) instead of 32 unrelated 16-byte pieces: ~DIM x fewer L1 requests per
-// gathered node.  Per-component partial sums are combined over the slots with a fixed shuffle tree.
-// Measured 2x slower in-cycle at config 5 (10.5 vs 5.0 ms: one row in flight per warp), so off.
-// ------------------------------------------------------------------------------------------------
-#ifndef SS_ROW_CL
-#define SS_ROW_CL 0
-#endif
-
-template <int DIM>
-__device__ __forceinline__ double2 cl_slot_sum(double2 v, int lane) {
-  // sum over lanes d, d+DIM, d+2 DIM, ... (< 32) into lane d; lanes >= NSLOT*DIM hold 0
-  constexpr int offs3[4] = {24, 12, 6, 3};
-  constexpr int offs2[4] = {16, 8, 4, 2};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int o = DIM == 3 ? offs3[i] : offs2[i];
-    const double tx = __shfl_down_sync(0xffffffffu, v.x, o);
-    const double ty = __shfl_down_sync(0xffffffffu, v.y, o);
-    if (lane + o < 32) { v.x += tx; v.y += ty; }
-  }
-  return v;
-}
-
-template <int DIM>
-__device__ __forceinline__ double2 saddle_vel_row_cl(const SsOperatorDev& op, int r, double omega,
-                                                     const double2* __restrict__ x, int lane, int xs) {
-  constexpr int NSLOT = 32 / DIM;
-  const int slot = lane / DIM, d = lane - slot * DIM;
-  double2 acc = make_double2(0.0, 0.0);
-  if (slot < NSLOT) {
-    const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-#pragma unroll 3
-    for (int e = e0 + slot; e < e1; e += NSLOT) {
-      const int B = __ldg(op.ncol + e);
-      const double2 a = __ldg(op.sm + e);
-      const double am = omega * a.y;
-      const double2 v = x[((size_t)B * DIM + d) * xs];
-      acc.x += a.x * v.x - am * v.y;
-      acc.y += a.x * v.y + am * v.x;
-    }
-    const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
-#pragma unroll 2
-    for (int e = p0 + slot; e < p1; e += NSLOT) {
-      const double2 v = x[(size_t)(op.nfv + __ldg(op.pcol + e)) * xs];
-      const double dv = __ldg(op.dp + (size_t)e * DIM + d);
-      acc.x += dv * v.x;
-      acc.y += dv * v.y;
-    }
-  }
-  return cl_slot_sum<DIM>(acc, lane);
-}
-
-template <int DIM>
-__device__ __forceinline__ double2 saddle_pres_row_cl(const SsOperatorDev& op, int j,
-                                                      const double2* __restrict__ x, int lane, int xs) {
-  constexpr int NSLOT = 32 / DIM;
-  const int slot = lane / DIM, d = lane - slot * DIM;
-  double2 acc = make_double2(0.0, 0.0);
-  if (slot < NSLOT) {
-    const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
-#pragma unroll 3
-    for (int e = e0 + slot; e < e1; e += NSLOT) {
-      const double dv = __ldg(op.dt + (size_t)e * DIM + d);
-      const double2 v = x[((size_t)__ldg(op.tcol + e) * DIM + d) * xs];
-      acc.x += dv * v.x;
-      acc.y += dv * v.y;
-    }
-  }
-  acc.x = warp_sum(acc.x);
-  acc.y = warp_sum(acc.y);
-  return acc;
-}
-
 // x is read with stride xs (xs = batch: one mode's column of the mode-interleaved P).
 template <int DIM, class Emit>
 __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, double omega,
                                              const double2* __restrict__ x, Emit&& emit, int xs = 1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nvb = saddle_nvb(op);
-#if SS_ROW_CL
-  if (blk < nvb) {
-#pragma unroll 1
-    for (int it = 0; it < SPMV_VROWS / 8; ++it) {
-      const int r = blk * SPMV_VROWS + it * 8 + warp;
-      if (r >= op.nfree) break;
-      const double2 v = saddle_vel_row_cl<DIM>(op, r, omega, x, lane, xs);
-      if (lane < DIM) emit(r * DIM + lane, v);
-    }
-  } else {
-    const int pb = blk - nvb;
-#pragma unroll 1
-    for (int it = 0; it < SPMV_PROWS / 8; ++it) {
-      const int j = pb * SPMV_PROWS + it * 8 + warp;
-      if (j >= op.npf) break;
-      const double2 v = saddle_pres_row_cl<DIM>(op, j, x, lane, xs);
-      if (lane == 0) emit(op.nfv + j, v);
-    }
-  }
-  return;
-#endif
   if (blk < nvb) {
     constexpr int RPW = 32 / ROW_LANES;   // rows per warp per iteration
     const int grp = lane / ROW_LANES, gl = lane % ROW_LANES;
