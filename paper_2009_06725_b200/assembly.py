@@ -346,16 +346,18 @@ class SaddleOperator:
                   _lib.dptr(u), _lib.dptr(p), _lib.stream_ptr(self.device))
         return u, p
 
-    def krylov(self, restart: int, nb: int, hist_cap: int):
-        """Cached batched-GMRES workspace with capacity >= nb modes."""
+    def krylov(self, restart: int, nb: int, hist_cap: int, slot: int = 0):
+        """Cached batched-GMRES workspace with capacity >= nb modes (``slot`` > 0: the extra
+        workspaces of concurrently solved sub-batches, krylov.concurrent_groups)."""
         from .krylov import KrylovWorkspace
 
-        ws = self._krylov.get(restart)
+        key = restart if slot == 0 else (restart, slot)
+        ws = self._krylov.get(key)
         if ws is None or ws.max_batch < nb or ws.hist_cap < hist_cap:
             if ws is not None:
                 ws.close()
             ws = KrylovWorkspace.for_operator(self, restart, nb, hist_cap)
-            self._krylov[restart] = ws
+            self._krylov[key] = ws
         return ws
 
     def release_workspaces(self):

@@ -289,17 +289,81 @@ def gmres_batched(batch, settings: SolverSettings, x0=None, keep_history=True):
             reps.extend(r)
         return torch.cat(xs, dim=0), reps
     jac = settings.preconditioner == "jacobi"
+    hist_cap = max(1, settings.max_iterations)
+    k = concurrent_groups(op.n, nb)
     with op.lock:
-        ws = op.krylov(settings.restart, nb, max(1, settings.max_iterations))
         wall0, cpu0 = time.perf_counter(), time.thread_time()
-        out = ws.solve(batch.omegas, batch.rhs, x0, settings.tolerance, settings.max_iterations, jacobi=jac)
+        if k == 1:
+            ws = op.krylov(settings.restart, nb, hist_cap)
+            out = ws.solve(batch.omegas, batch.rhs, x0, settings.tolerance, settings.max_iterations, jacobi=jac)
+            res = ws.residuals(nb)
+            hists = [ws.history(b, int(out["hist_len"][b])) if keep_history else [] for b in range(nb)]
+            X, iters, conv = out["x"], out["iterations"], out["converged"]
+        else:
+            X, iters, conv, res, hists = _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k)
         wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
-        res = ws.residuals(nb)
-        hists = [ws.history(b, int(out["hist_len"][b])) if keep_history else [] for b in range(nb)]
     reports = []
     for b in range(nb):
-        hist = hists[b]
-        reports.append(SolveReport(iterations=int(out["iterations"][b]), residual=float(res[b]),
-                                   converged=bool(out["converged"][b] and res[b] <= settings.tolerance),
-                                   wall_time=wall, cpu_time=cpu, residual_history=hist))
-    return out["x"], reports
+        reports.append(SolveReport(iterations=int(iters[b]), residual=float(res[b]),
+                                   converged=bool(conv[b] and res[b] <= settings.tolerance),
+                                   wall_time=wall, cpu_time=cpu, residual_history=hists[b]))
+    return X, reports
+
+
+def concurrent_groups(n: int, nb: int) -> int:
+    """Sub-batches run concurrently (own workspace, CUDA stream and host thread) for small systems:
+    each tick kernel of a small system leaves SMs idle in its latency tails, which the other
+    sub-batches fill (measured: 17 modes at n = 8 782 +24 % with 4 groups; 9 modes at n = 9 103
+    +4 %).  Per-mode results are bitwise independent of the grouping (batch invariance)."""
+    if n >= 200_000 or nb < 4:
+        return 1
+    return min(4, nb // 2)
+
+
+def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
+    import threading
+
+    torch = _lib.torch_mod()
+    nb = batch.nb
+    groups = [list(range(g, nb, k)) for g in range(k)]
+    wss = [op.krylov(settings.restart, len(g), hist_cap, slot=i) for i, g in enumerate(groups)]
+    rhs = [batch.rhs[g].contiguous() for g in groups]
+    x0s = [None if x0 is None else x0[g].contiguous() for g in groups]
+    torch.cuda.synchronize(op.device)
+    streams = [torch.cuda.Stream(op.device) for _ in groups]
+    outs, errs = [None] * k, [None] * k
+
+    def run(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                o = wss[i].solve(batch.omegas[groups[i]], rhs[i], x0s[i], settings.tolerance,
+                                 settings.max_iterations, jacobi=jac)
+                res = wss[i].residuals(len(groups[i]))
+                h = [wss[i].history(b, int(o["hist_len"][b])) if keep_history else [] for b in range(len(groups[i]))]
+                torch.cuda.current_stream().synchronize()
+                outs[i] = (o, res, h)
+        except BaseException as exc:   # re-raised in the caller's thread
+            errs[i] = exc
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(k)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    X = torch.empty((nb, op.ld), dtype=torch.complex128, device=op.device)
+    iters = np.zeros(nb, dtype=np.int64)
+    conv = np.zeros(nb, dtype=bool)
+    res = np.zeros(nb)
+    hists = [None] * nb
+    for i, g in enumerate(groups):
+        o, r, h = outs[i]
+        X[g] = o["x"]
+        iters[g] = o["iterations"]
+        conv[g] = o["converged"]
+        res[g] = r
+        for j, b in enumerate(g):
+            hists[b] = h[j]
+    return X, iters, conv, res, hists
