@@ -315,9 +315,9 @@ def concurrent_groups(n: int, nb: int) -> int:
     each tick kernel of a small system leaves SMs idle in its latency tails, which the other
     sub-batches fill (measured: 17 modes at n = 8 782 +24 % with 4 groups; 9 modes at n = 9 103
     +4 %).  Per-mode results are bitwise independent of the grouping (batch invariance)."""
-    if n >= 200_000 or nb < 4:
+    if n >= 200_000:
         return 1
-    return min(4, nb // 2)
+    return max(1, min(4, nb // 4))   # sub-batches of >= 4 modes (config 1: 4 groups of 2-3 measured -13 %)
 
 
 def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
