@@ -317,7 +317,7 @@ def concurrent_groups(n: int, nb: int) -> int:
     +4 %).  Per-mode results are bitwise independent of the grouping (batch invariance)."""
     if n >= 200_000:
         return 1
-    return max(1, min(4, nb // 4))   # sub-batches of >= 4 modes (config 1: 4 groups of 2-3 measured -13 %)
+    return max(1, min(4, nb // 3))   # sub-batches of >= 3 modes (config 1: 4 groups of 2-3 measured -13 %)
 
 
 def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
