@@ -71,9 +71,22 @@ def _ours(name):
 
 
 def _with_form_passthrough(fn, original):
-    """Device function for the full viscous form; the reference's original for any other form."""
+    """Device function for the full viscous form; the reference's original for any other form
+    (``viscous_form`` given by keyword or position, per the reference's own signature)."""
+    import inspect
+
+    try:
+        sig = inspect.signature(original if original is not None else fn)
+    except (TypeError, ValueError):
+        sig = None
+
     def wrapper(*args, **kwargs):
         form = kwargs.get("viscous_form", "full")
+        if sig is not None and "viscous_form" not in kwargs:
+            try:
+                form = sig.bind_partial(*args, **kwargs).arguments.get("viscous_form", "full")
+            except TypeError:
+                pass
         if form != "full" and original is not None:
             return original(*args, **kwargs)
         return fn(*args, **kwargs)

@@ -53,6 +53,18 @@ def test_overlay_replaces_hot_path_and_shares_exception_types(reference_on_path)
     for name in ("solve_modes", "assemble_mode_system", "adaptive_mode_refinement"):
         assert getattr(spectralstokes, name).__wrapped__ is getattr(b2, name)
     assert spectralstokes.runner.solve_modes.__wrapped__ is b2.spectral.solve_modes
+    # the out-of-scope "symmetric" viscous form goes to the reference's own function, whether
+    # passed by keyword or by position
+    calls = []
+    wrapped = spectralstokes.spectral._solve_one_mode
+    orig = dropin._state["patched"]
+    prev = next(p for m, n, p in orig if m is spectralstokes.spectral and n == "_solve_one_mode")
+    import functools
+
+    spy = functools.wraps(prev)(lambda *a, **k: calls.append((a, k)) or "ref")
+    w2 = dropin._with_form_passthrough(wrapped.__wrapped__, spy)
+    assert w2(None, None, None, None, 1, "symmetric") == "ref"
+    assert w2(None, None, None, None, 1, viscous_form="symmetric") == "ref" and len(calls) == 2
     # the MSS time-domain path bound gmres at import and stays on the reference's CPU code
     assert spectralstokes.timedomain.gmres is not b2.krylov.gmres
     # exceptions raised by this package are the reference's classes
