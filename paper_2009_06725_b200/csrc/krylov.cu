@@ -80,8 +80,6 @@ struct KArgs {
   int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
   int wide;                    // restart > WIDE_RESTART: basis passes without the shared-memory ring (any J)
   int stream_spmv;             // row layout: TMA-staged persistent SpMV (1) or one CTA per row block (0)
-  int row_contig;              // row layout: 0 round-robin blocks, 1 contiguous run per CTA, 2 per-SM interleave
-  int nsm;                     // multiprocessors of the device
 };
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
@@ -387,24 +385,7 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
     // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
     // the mode's column of P with stride pstride.  Grid-stride over the row blocks (a few CTAs per
     // SM): the mode-state prologue and the last-CTA election are paid per CTA, not per block.
-    // row_contig: each CTA walks one contiguous run of row blocks (neighbouring rows share x lines
-    // in L1); otherwise blocks are dealt round-robin over the CTAs
-    // row_contig == 2: the CTAs that share an SM (blockIdx = sm + nsm * j under the usual
-    // round-robin placement) interleave over one contiguous range of blocks, so the 4 resident on
-    // an SM work on neighbouring rows at the same time (every block still has exactly one owner)
-    int b0, b1, bstep;
-    if (a.row_contig == 2 && gridDim.x % a.nsm == 0) {
-      const int per_sm = (a.nsb + a.nsm - 1) / a.nsm;
-      const int sm = blockIdx.x % a.nsm, j = blockIdx.x / a.nsm;
-      b0 = sm * per_sm + j;
-      b1 = min(a.nsb, (sm + 1) * per_sm);
-      bstep = gridDim.x / a.nsm;
-    } else {
-      const int per = a.row_contig ? (a.nsb + gridDim.x - 1) / gridDim.x : 1;
-      b0 = a.row_contig ? blockIdx.x * per : blockIdx.x;
-      b1 = a.row_contig ? min(a.nsb, b0 + per) : a.nsb;
-      bstep = a.row_contig ? 1 : gridDim.x;
-    }
+    const int b0 = blockIdx.x, b1 = a.nsb, bstep = gridDim.x;   // blocks dealt round-robin (measured best)
     for (int blk = b0; blk < b1; blk += bstep) {
       if (s_any_inner)
         for (int b = 0; b < a.nb; ++b) {
@@ -1186,9 +1167,7 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     K->stream_ctas = 2 * sms;
     K->row_ctas = 16 * sms;
     if (const char* e = getenv("SS_ROW_CTAS")) K->row_ctas = std::max(1, atoi(e));
-    K->a.row_contig = 0;
-    K->a.nsm = sms;
-    if (const char* e = getenv("SS_ROW_CONTIG")) K->a.row_contig = atoi(e);
+
     if (const char* e = getenv("SS_STREAM_CTAS")) K->stream_ctas = std::max(1, atoi(e));
     K->a.stream_spmv = 0;   // measured slower than the per-block row kernel at config 5
     if (const char* e = getenv("SS_SPMV_STREAM")) K->a.stream_spmv = atoi(e);
