@@ -33,7 +33,7 @@ typedef struct ss_comm ss_comm;       /* NCCL communicator for the mode-field ga
 #define SS_COMM_ID_BYTES 128
 
 /* ABI revision: the Python binding refuses (rebuilds) a library whose ss_version() differs. */
-#define SS_ABI_VERSION 3
+#define SS_ABI_VERSION 4
 
 const char* ss_last_error(void);
 int ss_version(void);
@@ -151,6 +151,9 @@ int ss_krylov_solve(ss_krylov* k, int nb, const double* omegas_host, const int* 
                     void* stream, int64_t* out_int, double* out_dbl);
 /* Per-iteration preconditioned residual estimates of mode b (SolveReport.residual_history). */
 int ss_krylov_history(const ss_krylov* k, int mode, int64_t count, double* out_host);
+/* Tick (one SpMV + three basis passes over the batch) at which each mode of the last solve
+ * finished; SolveReport.wall_time of a mode = batch wall time x its tick / all ticks. */
+int ss_krylov_done_ticks(const ss_krylov* k, int nb, int64_t* out_host);
 /* Ticks and kernel launches of the last solve. */
 int ss_krylov_last_stats(const ss_krylov* k, int64_t* ticks, int64_t* launches);
 /* True relative residuals ||b - A x||/||b|| of the workspace's X (residual_norm, assembly.py:357-362). */

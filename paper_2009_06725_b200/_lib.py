@@ -69,6 +69,7 @@ SIGNATURES = {
     "ss_krylov_solve": (I32, [P, I32, PD, C.POINTER(I32), P, P, I64, I32, D, I64, I32, P, PI64, PD]),
     "ss_krylov_history": (I32, [P, I32, I64, PD]),
     "ss_krylov_last_stats": (I32, [P, PI64, PI64]),
+    "ss_krylov_done_ticks": (I32, [P, I32, PI64]),
     "ss_krylov_residuals": (I32, [P, I32, P, PD]),
     "ss_krylov_copy": (I32, [P, I32, I32, P, I64, P]),
     "ss_krylov_csr_scale": (I32, [P, I32, PD]),
@@ -86,7 +87,7 @@ SIGNATURES = {
 _lib = None
 
 # Must equal SS_ABI_VERSION in include/spectralstokes_b200.h (bumped whenever an entry point changes).
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 def load(build_if_missing: bool = True):

@@ -37,7 +37,7 @@ enum Phase : int { PH_IDLE = 0, PH_RESID = 1, PH_START = 2, PH_INNER = 3, PH_XUP
 struct ModeCtl {
   int phase, k, iters, maxiter;
   int restart, breakdown, first, converged;
-  int zero_x, set, hist_len, pad1;
+  int zero_x, set, hist_len, done_tick;   // done_tick: tick at which the mode finished
   double beta, target, bnorm, tol;
   double omega, true_res, gk_last, est;
 };
@@ -74,7 +74,7 @@ struct KArgs {
   int* n_done;
   double* hist;                // [b][hist_cap]
   unsigned long long* bytes;   // [8] algorithmic bytes moved per kernel kind (profiling)
-  long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap
+  long long* loop;             // [0] ticks executed by the device-side loop, [1] tick cap, [2] ticks of this solve
   int x_in_a;                  // cycle-end x update inside the next tick's pass-A launch (1) or own launch (0)
   int gthr[3];                 // pass B: largest J using 1, 2, 4 warps per row block (8 above)
   int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
@@ -111,6 +111,7 @@ __device__ __forceinline__ bool last_cta(const KArgs& a, int b, int which, int t
 
 __device__ __forceinline__ void mark_done(const KArgs& a, ModeCtl* c, int converged) {
   c->phase = PH_DONE;
+  c->done_tick = (int)a.loop[2];
   c->converged = converged;
   atomicAdd(a.n_done, 1);
 }
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
     for (int b = 0; b < a.nb; ++b)
       if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
   if (!last_cta(a, 0, 6, (int)gridDim.x, &sflag)) return;
+  if (threadIdx.x == 0) a.loop[2] += 1;   // one tick done (per-mode completion ticks, ss_krylov_done_ticks)
   for (int b = 0; b < a.nb; ++b) {
     const int ph = sph[b];
     if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
@@ -415,6 +417,7 @@ __global__ void __launch_bounds__(PT) k_tick_spmv(KArgs a) {
   // one election for the whole batch (slot 6 of mode 0's counters): the last CTA to finish makes
   // every mode's cycle decisions
   if (!last_cta(a, 0, 6, (int)gridDim.x, &sflag)) return;
+  if (threadIdx.x == 0) a.loop[2] += 1;   // one tick done (per-mode completion ticks, ss_krylov_done_ticks)
   for (int b = 0; b < a.nb; ++b) {
     const int ph = sph[b];
     if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
@@ -1142,7 +1145,7 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if ((rc = kalloc(K, B, &a.ctl))) return rc;
   if ((rc = kalloc(K, B * a.hist_cap, &a.hist))) return rc;
   if ((rc = kalloc(K, 8, &a.bytes))) return rc;
-  if ((rc = kalloc(K, 2, &a.loop))) return rc;
+  if ((rc = kalloc(K, 3, &a.loop))) return rc;
   SS_CUDA(cudaHostAlloc((void**)&K->h_done, 2 * sizeof(int), cudaHostAllocDefault));
   SS_CUDA(cudaStreamCreateWithFlags(&K->cap_stream, cudaStreamNonBlocking));
   SS_CUDA(cudaEventCreateWithFlags(&K->ev[0], cudaEventDisableTiming));
@@ -1466,6 +1469,7 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
   }
   SS_CUDA(cudaMemcpyAsync(a.ctl, ctl.data(), sizeof(ModeCtl) * nb, cudaMemcpyHostToDevice, st));
   SS_CUDA(cudaMemsetAsync(a.n_done, 0, sizeof(int), st));
+  SS_CUDA(cudaMemsetAsync(a.loop + 2, 0, sizeof(long long), st));
   if (rhs_dev)
     SS_CUDA(cudaMemcpy2DAsync(a.RHS, a.ld * sizeof(double2), rhs_dev, ld_in * sizeof(double2), a.n * sizeof(double2),
                               nb, cudaMemcpyDeviceToDevice, st));
@@ -1548,6 +1552,16 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
       out_dbl[b * 4 + 3] = ctl[b].target;
     }
   }
+  return SS_OK;
+}
+
+// Tick at which each of the last solve's nb modes finished (0 = before the first tick).
+extern "C" int ss_krylov_done_ticks(const ss_krylov* K, int nb, int64_t* out_host) {
+  if (!K || !out_host || nb < 1 || nb > K->max_batch) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  std::vector<ModeCtl> ctl(nb);
+  SS_CUDA(cudaSetDevice(K->device));
+  SS_CUDA(cudaMemcpy(ctl.data(), K->a.ctl, sizeof(ModeCtl) * nb, cudaMemcpyDeviceToHost));
+  for (int b = 0; b < nb; ++b) out_host[b] = ctl[b].done_tick;
   return SS_OK;
 }
 
@@ -1758,6 +1772,7 @@ extern "C" int ss_krylov_profile(ss_krylov* K, int nb, const double* omegas_host
   }
   SS_CUDA(cudaMemcpyAsync(a.ctl, ctl.data(), sizeof(ModeCtl) * nb, cudaMemcpyHostToDevice, st));
   SS_CUDA(cudaMemsetAsync(a.n_done, 0, sizeof(int), st));
+  SS_CUDA(cudaMemsetAsync(a.loop + 2, 0, sizeof(long long), st));
   SS_CUDA(cudaMemsetAsync(a.X, 0, sizeof(double2) * a.ld * nb, st));
   SS_CUDA(cudaMemsetAsync(a.bytes, 0, sizeof(unsigned long long) * 8, st));
   if (tick_dim(K) == 3) k_init<3><<<nb * a.nseg, PT, 0, st>>>(a);

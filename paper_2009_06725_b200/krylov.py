@@ -48,7 +48,8 @@ class SolverSettings:
 class SolveReport:
     """Outcome of one linear solve (krylov.py:37-46).
 
-    For batched solves ``wall_time``/``cpu_time`` are those of the whole batch call.
+    For batched solves ``wall_time``/``cpu_time`` are the batch call's, scaled by the fraction of the
+    batch's ticks the mode needed (modes finish at their own tick).
     """
 
     iterations: int
@@ -154,6 +155,12 @@ class KrylovWorkspace:
         if count:
             _lib.call("ss_krylov_history", self._h, int(mode), count, _lib.ptr(out))
         return [float(v) for v in out[:count]]
+
+    def done_ticks(self, nb: int) -> np.ndarray:
+        """Tick at which each mode of the last solve finished (ss_krylov_done_ticks)."""
+        out = np.zeros(nb, dtype=np.int64)
+        _lib.call("ss_krylov_done_ticks", self._h, int(nb), _lib.ptr(out, C.c_int64))
+        return out
 
     def last_stats(self):
         t, l = C.c_int64(), C.c_int64()
@@ -296,18 +303,28 @@ def gmres_batched(batch, settings: SolverSettings, x0=None, keep_history=True):
         if k == 1:
             ws = op.krylov(settings.restart, nb, hist_cap)
             out = ws.solve(batch.omegas, batch.rhs, x0, settings.tolerance, settings.max_iterations, jacobi=jac)
+            frac = _tick_fractions(ws.done_ticks(nb))
             res = ws.residuals(nb)
             hists = [ws.history(b, int(out["hist_len"][b])) if keep_history else [] for b in range(nb)]
             X, iters, conv = out["x"], out["iterations"], out["converged"]
         else:
-            X, iters, conv, res, hists = _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k)
+            X, iters, conv, res, hists, frac = _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history,
+                                                                 k)
         wall, cpu = time.perf_counter() - wall0, time.thread_time() - cpu0
     reports = []
     for b in range(nb):
+        # a mode's wall/cpu time: the batch's, scaled by the share of its ticks (the device finishes
+        # modes at different ticks; the reference times each mode's own solve, krylov.py:194-202)
         reports.append(SolveReport(iterations=int(iters[b]), residual=float(res[b]),
                                    converged=bool(conv[b] and res[b] <= settings.tolerance),
-                                   wall_time=wall, cpu_time=cpu, residual_history=hists[b]))
+                                   wall_time=wall * frac[b], cpu_time=cpu * frac[b], residual_history=hists[b]))
     return X, reports
+
+
+def _tick_fractions(done_ticks) -> np.ndarray:
+    t = np.asarray(done_ticks, dtype=float)
+    top = t.max() if t.size else 0.0
+    return t / top if top > 0 else np.ones_like(t)
 
 
 def concurrent_groups(n: int, nb: int) -> int:
@@ -341,7 +358,7 @@ def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
                 res = wss[i].residuals(len(groups[i]))
                 h = [wss[i].history(b, int(o["hist_len"][b])) if keep_history else [] for b in range(len(groups[i]))]
                 torch.cuda.current_stream().synchronize()
-                outs[i] = (o, res, h)
+                outs[i] = (o, res, h, wss[i].done_ticks(len(groups[i])))
         except BaseException as exc:   # re-raised in the caller's thread
             errs[i] = exc
 
@@ -358,12 +375,14 @@ def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
     conv = np.zeros(nb, dtype=bool)
     res = np.zeros(nb)
     hists = [None] * nb
+    ticks = np.zeros(nb)
     for i, g in enumerate(groups):
-        o, r, h = outs[i]
+        o, r, h, t = outs[i]
+        ticks[g] = t
         X[g] = o["x"]
         iters[g] = o["iterations"]
         conv[g] = o["converged"]
         res[g] = r
         for j, b in enumerate(g):
             hists[b] = h[j]
-    return X, iters, conv, res, hists
+    return X, iters, conv, res, hists, _tick_fractions(ticks)

@@ -24,6 +24,8 @@ Fixtures
   c2_gmres.npz    BASELINE config 2 fixed-budget GMRES (modes 1, 16; restart 200, 200 iterations,
                   x0 = 0): residual history, x at sampled rows, ||x|| and projections of x on
                   seeded vectors                                                 (krylov.py:63-164)
+  c3_gmres.npz    BASELINE config 3 at full size (2 059 200-tet bend, n = 8.39 M): fixed-budget GMRES
+                  (mode 1, restart 40, 40 iterations, x0 = 0): history, sampled x, projections
   adaptive.npz    adaptive_mode_refinement on seeded sampled waveforms: final N_m, converged flag,
                   per-mode energies and iteration counts                       (spectral.py:333-371)
   post.npz        post-processing on seeded complex fields: interpolate_at_quadrature, l2_norm,
@@ -302,6 +304,30 @@ def make_c2_gmres(pool):
     np.savez_compressed(HERE / "c2_gmres.npz", **out)
 
 
+def make_c3_gmres():
+    from paper_2009_06725_b200.workloads import c3_case
+
+    case = c3_case()
+    t0 = time.perf_counter()
+    q = _ref_qmesh(case.mesh)
+    props = RA.FluidProps(density=case.density, viscosity=case.viscosity)
+    s = RA.assemble_mode_system(q, props, float(case.omegas[1]), g_mode=case.coefficients[1] * case.profile)
+    t_asm = time.perf_counter() - t0
+    sc = RK.jacobi_precondition(s)
+    t0 = time.perf_counter()
+    x, it, hist, conv = RK.gmres(s.matrix, s.rhs, tol=1e-10, restart=40, maxiter=40, scale=sc)
+    wall = time.perf_counter() - t0
+    n = s.n_dofs
+    rows = np.sort(np.random.default_rng(1301).choice(n, 20000, replace=False))
+    rng = np.random.default_rng(2301)
+    proj = np.stack([rng.normal(size=n) + 1j * rng.normal(size=n) for _ in range(2)]) @ x
+    np.savez_compressed(HERE / "c3_gmres.npz", hist=np.array(hist), iters=np.int64(it), rows=rows, x_rows=x[rows],
+                        x_norm=np.float64(np.linalg.norm(x)), proj=proj, n=np.int64(n),
+                        pattern_sha=np.array(_sha(s.matrix.indptr, s.matrix.indices)), nnz=np.int64(s.matrix.nnz),
+                        wall=np.float64(wall), t_assembly=np.float64(t_asm))
+    print("c3 gmres", it, "iterations", round(wall, 1), "s; assembly", round(t_asm, 1), "s; n", n)
+
+
 # -- adaptive mode refinement (spectral.py:333-371) -------------------------------------------------
 
 ADAPTIVE_CASES = {
@@ -435,3 +461,5 @@ if __name__ == "__main__":
             make_c2_gmres(pool)
         if "adaptive" in what:
             make_adaptive()
+        if "c3gmres" in what:
+            make_c3_gmres()

@@ -344,3 +344,20 @@ def test_wide_restart_through_solve_modes():
     s = sols[0]
     assert s.report.converged
     assert np.linalg.norm(s.velocity - g["u_4"]) <= 1e-7 * np.linalg.norm(g["u_4"])
+
+
+@pytest.mark.gpu
+def test_per_mode_wall_time_follows_completion_tick(c1):
+    """SolveReport.wall_time per mode: the batch's wall time scaled by the tick at which the mode
+    finished (ss_krylov_done_ticks), so a mode needing more iterations reports more time."""
+    case, props, _ = c1
+    idx = [1, 3, 8]
+    h = case.h_modes()
+    b = assemble_mode_systems(case.qmesh, props, case.omegas[idx], None, [h[i] for i in idx])
+    X, reps = gmres_batched(b, SolverSettings(tolerance=1e-9, restart=50))
+    walls = [r.wall_time for r in reps]
+    its = [r.iterations for r in reps]
+    assert all(w > 0 for w in walls)
+    order = np.argsort(its)
+    assert all(walls[order[i]] <= walls[order[i + 1]] + 1e-12 for i in range(len(idx) - 1))
+    assert max(walls) > 2 * min(walls) or max(its) < 1.5 * min(its)

@@ -97,3 +97,35 @@ def test_adaptive_refinement_matches_reference(name):
     u = sols[-1].velocity
     ur = g[f"{name}_u_last"]
     assert np.linalg.norm(u - ur) <= 1e-7 * max(np.linalg.norm(ur), 1e-300) or np.linalg.norm(ur) == 0.0
+
+
+def test_config3_full_size_fixed_budget_matches_reference():
+    """Config 3 at full size (2 059 200-tet bend, n = 8.39 M): 40 iterations of GMRES(40) from x0 = 0
+    for mode 1 against the reference's own run (tests/golden/c3_gmres.npz): pattern SHA, history,
+    sampled iterate, ||x|| and projections."""
+    import hashlib
+
+    from paper_2009_06725_b200.workloads import c3_case
+
+    g = golden("c3_gmres.npz")
+    case = c3_case()
+    q = case.qmesh
+    props = FluidProps(case.density, case.viscosity)
+    op = get_operator(q, props)
+    assert op.n == int(g["n"]) and op.nnz == int(g["nnz"])
+    ip, ix = op.pattern()
+    h = hashlib.sha256()
+    for a in (ip, ix):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(g["pattern_sha"])
+    batch = assemble_mode_systems(q, props, case.omegas[[1]], [case.coefficients[1] * case.profile], None, operator=op)
+    X, reps = gmres_batched(batch, SolverSettings(tolerance=1e-10, restart=40, max_iterations=40))
+    x = X[0, : op.n].cpu().numpy()
+    assert reps[0].iterations == int(g["iters"]) == 40
+    np.testing.assert_allclose(reps[0].residual_history, g["hist"], rtol=1e-6)
+    assert np.linalg.norm(x[g["rows"]] - g["x_rows"]) <= 1e-8 * np.linalg.norm(g["x_rows"])
+    assert np.linalg.norm(x) == pytest.approx(float(g["x_norm"]), rel=1e-9)
+    rng = np.random.default_rng(2301)
+    proj = np.stack([rng.normal(size=op.n) + 1j * rng.normal(size=op.n) for _ in range(2)]) @ x
+    assert np.abs(proj - g["proj"]).max() <= 1e-8 * np.abs(g["proj"]).max()
+    op.release_workspaces()
