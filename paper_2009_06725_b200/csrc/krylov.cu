@@ -598,7 +598,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
 // split the columns) instead of through the shared-memory ring, whose stage must hold a whole
 // J x 32 block.  Dots are taken in tiles of 256 columns (32 register accumulators per thread).
 // Coefficients come from global memory: B/C: qs_j * C{1,2}_j, X: Y_j.
-template <int PASS, int TT = PT / 8>
+template <int PASS>
 __device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s, int J, int k, double2* red,
                                                     double2* part) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -640,15 +640,15 @@ __device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s
     }
   }
   if (PASS == PASS_A || PASS == PASS_B) {
-    for (int j0 = 0; j0 < J; j0 += 8 * TT) {
-      double2 acc[TT];
+    for (int j0 = 0; j0 < J; j0 += PT) {
+      double2 acc[PT / 8];
 #pragma unroll
-      for (int t = 0; t < TT; ++t) acc[t] = make_double2(0.0, 0.0);
+      for (int t = 0; t < PT / 8; ++t) acc[t] = make_double2(0.0, 0.0);
       for (int blk = blk_begin; blk < blk_end; ++blk) {
         const double2 v = vec[(int64_t)blk * RB + lane];
         const double2* S = qblock(a, b, blk) + lane;
 #pragma unroll
-        for (int t = 0; t < TT; ++t) {
+        for (int t = 0; t < PT / 8; ++t) {
           const int j = j0 + warp + 8 * t;
           if (j < J) {
             const double2 q = S[(size_t)j * RB];
@@ -658,7 +658,7 @@ __device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s
         }
       }
 #pragma unroll
-      for (int t = 0; t < TT; ++t) {
+      for (int t = 0; t < PT / 8; ++t) {
         const int j = j0 + warp + 8 * t;
         const double x = warp_sum(acc[t].x), y = warp_sum(acc[t].y);
         if (lane == 0 && j < J) part[j] = make_double2(x, y);
@@ -801,11 +801,8 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
   }
 }
 
-// The body of a basis pass.  WIDE_ONLY: the small-n instantiation that always takes the
-// global-memory (wide) streaming path, launched without the shared-memory ring at several CTAs
-// per SM (dots in 32-column tiles to keep registers low).
-template <int PASS, bool WIDE_ONLY>
-__device__ __forceinline__ void pass_body(const KArgs& a) {
+template <int PASS>
+__global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   extern __shared__ __align__(128) double2 smem[];
   __shared__ double2 coef[256];
   __shared__ double2 red[PASS == PASS_B ? 2 * PT : PT];
@@ -818,7 +815,7 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
   if (PASS == PASS_A && phase == PH_XUPDATE && a.x_in_a) {
     // cycle-end x += Q y rides on the next tick's pass-A launch (one launch per tick saved)
     const int kx = c->k;
-    if (WIDE_ONLY || a.wide) {
+    if (a.wide) {
       stream_segment_wide<PASS_X>(a, b, s, kx, kx, red, nullptr);
     } else {
       for (int j = tid; j < kx; j += PT) coef[j] = a.Y[(size_t)b * a.jcap + j];
@@ -835,9 +832,7 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
   double* qs = a.qs + (size_t)b * a.jcap;
   double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
   const int T = (J + 7) / 8;
-  if (WIDE_ONLY) {
-    stream_segment_wide<PASS, 4>(a, b, s, J, k, red, part);
-  } else if (a.wide) {
+  if (a.wide) {
     stream_segment_wide<PASS>(a, b, s, J, k, red, part);
   } else {
   // coefficients of the update (qs folded in): B: qs_j c_j, C: qs_j c2_j, X: y_j (already scaled)
@@ -919,16 +914,15 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
   if (PASS == PASS_A || PASS == PASS_B) return;
   // PASS_C: Givens update (krylov.py:115-149).  The H column and the stored rotations are staged
   // in (now idle) shared memory by all threads; one thread runs the serial recurrence on them.
-  const bool wide_ = WIDE_ONLY || a.wide;   // staging in global memory (no shared-memory ring)
   __shared__ double2 ys[256];
   __shared__ int s_solve;
   const int jc = a.jcap;
   // wide restart: the column, rotations and y live in global memory (H column k, CS, SN, Y)
   double2* hcol = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
-  double2* hs = wide_ ? hcol : smem;                           // column k (k+2 entries)
-  const double2* css = wide_ ? a.CS + (size_t)b * a.restart : smem + 256;   // cs[0..k)
-  const double2* sns = wide_ ? a.SN + (size_t)b * a.restart : smem + 512;   // sn[0..k)
-  double2* y = wide_ ? a.Y + (size_t)b * jc : ys;
+  double2* hs = a.wide ? hcol : smem;                           // column k (k+2 entries)
+  const double2* css = a.wide ? a.CS + (size_t)b * a.restart : smem + 256;   // cs[0..k)
+  const double2* sns = a.wide ? a.SN + (size_t)b * a.restart : smem + 512;   // sn[0..k)
+  double2* y = a.wide ? a.Y + (size_t)b * jc : ys;
   {
     const double2* c1 = a.C1 + (size_t)b * jc;
     const double2* c2 = a.C2 + (size_t)b * jc;
@@ -936,7 +930,7 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
     const double2* sng = a.SN + (size_t)b * a.restart;
     for (int i = tid; i <= k; i += PT) {
       hs[i] = cadd(c1[i], c2[i]);
-      if (i < k && !wide_) { smem[256 + i] = csg[i]; smem[512 + i] = sng[i]; }
+      if (i < k && !a.wide) { smem[256 + i] = csg[i]; smem[512 + i] = sng[i]; }
     }
   }
   __syncthreads();
@@ -1000,7 +994,7 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
     }
   }
   __syncthreads();
-  if (!wide_)
+  if (!a.wide)
     for (int i = tid; i <= k + 1; i += PT) hcol[i] = hs[i];
   __syncthreads();
   const int kk = s_solve;
@@ -1020,17 +1014,6 @@ __device__ __forceinline__ void pass_body(const KArgs& a) {
   for (int i = tid; i < kk; i += PT) a.Y[(size_t)b * jc + i] = cscale(y[i], qs[i]);   // in place when wide
   __syncthreads();
   if (tid == 0) c->phase = PH_XUPDATE;
-}
-
-template <int PASS>
-__global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
-  pass_body<PASS, false>(a);
-}
-
-// Small-n passes (small_wide): global-memory streaming, no dynamic shared memory, several CTAs per SM.
-template <int PASS>
-__global__ void __launch_bounds__(PT, 4) k_pass_w(KArgs a) {
-  pass_body<PASS, true>(a);
 }
 
 __global__ void k_finalize(KArgs a) {
@@ -1099,7 +1082,6 @@ struct ss_krylov {
   int64_t last_launches = 0;
   double2* csr_vals_owned = nullptr;
   int stream_ctas = 2 * 148;   // persistent CTAs of the staged tick SpMV (2 per SM)
-  int small_wide = 0;          // basis passes through k_pass_w (global-memory streaming, 4 CTAs per SM)
   int row_ctas = 16 * 148;     // grid-stride CTAs of the row-layout tick SpMV
 };
 
@@ -1194,7 +1176,6 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     if (const char* e = getenv("SS_SPMV_STREAM")) K->a.stream_spmv = atoi(e);
   }
   K->ticks_per_graph = n < 200000 ? 16 : 2;
-  if (const char* e = getenv("SS_WIDE_N")) K->small_wide = n < atoll(e) ? 1 : 0;
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
   K->a.x_in_a = 1;
   K->a.gthr[0] = 16;
@@ -1371,19 +1352,6 @@ static int launch_tick(ss_krylov* K, const KArgs& a, cudaStream_t st) {
   else if (a.kind == 0 && a.row_spmv) k_tick_spmv<DIM, 1><<<sgrid, PT, 0, st>>>(a);
   else k_tick_spmv<DIM, 0><<<sgrid, PT, 0, st>>>(a);
   SS_LAUNCH_CHECK();
-  if (K->small_wide) {
-    k_pass_w<PASS_A><<<gs, PT, 0, st>>>(a);
-    SS_LAUNCH_CHECK();
-    k_pass_w<PASS_B><<<gs, PT, 0, st>>>(a);
-    SS_LAUNCH_CHECK();
-    k_pass_w<PASS_C><<<gs, PT, 0, st>>>(a);
-    SS_LAUNCH_CHECK();
-    if (!a.x_in_a) {
-      k_pass_w<PASS_X><<<gs, PT, 0, st>>>(a);
-      SS_LAUNCH_CHECK();
-    }
-    return SS_OK;
-  }
   k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
   SS_LAUNCH_CHECK();
   k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
@@ -1748,21 +1716,17 @@ static int profile_ticks(ss_krylov* K, const KArgs& a, cudaStream_t st, int64_t 
     else k_tick_spmv<DIM, 0><<<sgrid, PT, 0, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[1], st));
-    if (K->small_wide) k_pass_w<PASS_A><<<gs, PT, 0, st>>>(a);
-    else k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
+    k_pass<PASS_A><<<gs, PT, K->smem_pass, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[2], st));
-    if (K->small_wide) k_pass_w<PASS_B><<<gs, PT, 0, st>>>(a);
-    else k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
+    k_pass<PASS_B><<<gs, PT, K->smem_pass, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[3], st));
-    if (K->small_wide) k_pass_w<PASS_C><<<gs, PT, 0, st>>>(a);
-    else k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
+    k_pass<PASS_C><<<gs, PT, K->smem_pass, st>>>(a);
     SS_LAUNCH_CHECK();
     SS_CUDA(cudaEventRecord(ev[4], st));
     if (!a.x_in_a) {
-      if (K->small_wide) k_pass_w<PASS_X><<<gs, PT, 0, st>>>(a);
-    else k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
+      k_pass<PASS_X><<<gs, PT, K->smem_pass, st>>>(a);
       SS_LAUNCH_CHECK();
     }
     SS_CUDA(cudaEventRecord(ev[5], st));
