@@ -361,3 +361,32 @@ def test_per_mode_wall_time_follows_completion_tick(c1):
     order = np.argsort(its)
     assert all(walls[order[i]] <= walls[order[i + 1]] + 1e-12 for i in range(len(idx) - 1))
     assert max(walls) > 2 * min(walls) or max(its) < 1.5 * min(its)
+
+
+@pytest.mark.gpu
+def test_maximum_batch_with_zero_and_steady_modes(small_channel_qmesh, fluid):
+    """MAX_BATCH (256) modes in one call -- steady (omega = 0), zero right-hand sides and ordinary
+    modes mixed, solved as concurrent sub-batches -- each equal bit for bit to its own one-mode
+    solve (batch invariance at the maximum batch)."""
+    from paper_2009_06725_b200.krylov import MAX_BATCH, concurrent_groups
+
+    q = small_channel_qmesh
+    nb = MAX_BATCH
+    rng = np.random.default_rng(12)
+    omegas = np.where(np.arange(nb) % 17 == 0, 0.0, rng.uniform(0.0, 40.0, nb))
+    amp = rng.normal(size=nb) + 1j * rng.normal(size=nb)
+    amp[5::31] = 0.0                                   # zero traction -> zero rhs -> early return
+    h = [{"inlet": a * np.array([1.0, 0.0], complex)} for a in amp]
+    settings = SolverSettings(tolerance=1e-8, restart=30, max_iterations=3000)
+    batch = assemble_mode_systems(q, fluid, omegas, None, h)
+    assert concurrent_groups(batch.operator.n, nb) > 1
+    X, reps = gmres_batched(batch, settings)
+    X = X.cpu().numpy()
+    for b in list(range(0, nb, 23)) + [5, 36]:
+        one = assemble_mode_systems(q, fluid, omegas[[b]], None, [h[b]])
+        Xs, rs = gmres_batched(one, settings)
+        assert np.array_equal(X[b], Xs.cpu().numpy()[0]), b
+        assert reps[b].iterations == rs[0].iterations
+    for b in range(5, nb, 31):
+        assert reps[b].iterations == 0 and reps[b].converged and not np.any(X[b])
+    assert all(r.converged for r in reps)
