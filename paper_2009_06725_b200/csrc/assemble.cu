@@ -418,11 +418,13 @@ extern "C" int ss_jacobi(const ss_pattern* P, int nb, const double* omegas_dev, 
 // Standalone mode-batched SpMV: Y[b] = s_b (.) (A(w_b) X[b])   (s = 1 unless jacobi)
 // One warp per node row (all dim components) or pressure row; blockIdx.y = mode.
 // ------------------------------------------------------------------------------------------------
-#ifndef SS_SPMV_MINB
-#define SS_SPMV_MINB 1
+#ifdef SS_SPMV_MINB
+#define SS_SPMV_BOUNDS __launch_bounds__(256, SS_SPMV_MINB)
+#else
+#define SS_SPMV_BOUNDS __launch_bounds__(256)
 #endif
 template <int DIM>
-__global__ void __launch_bounds__(256, SS_SPMV_MINB) k_spmv_saddle(SsOperatorDev op, int nb, const double* __restrict__ omegas,
+__global__ void SS_SPMV_BOUNDS k_spmv_saddle(SsOperatorDev op, int nb, const double* __restrict__ omegas,
                                                      const double2* __restrict__ X, double2* __restrict__ Y,
                                                      int64_t ld, int jacobi) {
   // one CTA = one row block for every mode: the block's matrix slice is re-read from L1

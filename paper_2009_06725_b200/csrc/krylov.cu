@@ -365,11 +365,15 @@ __global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
 // One CTA = one row block, all modes of the batch.  ROW: the row-layout INNER SpMV (8 lanes per
 // node row, the mode's strided column of P), instantiated separately so its register allocation is
 // not shaped by the mode-interleaved kernel.
-#ifndef SS_TICK_MINB
-#define SS_TICK_MINB 1
+// Launch bounds: maxThreads only (ptxas then keeps these kernels at 64 registers, 4 CTAs per SM;
+// an explicit minBlocks of 1 lets it take ~128 and costs 1.5x in-cycle at config 5).
+#ifdef SS_TICK_MINB
+#define SS_TICK_BOUNDS __launch_bounds__(PT, SS_TICK_MINB)
+#else
+#define SS_TICK_BOUNDS __launch_bounds__(PT)
 #endif
 template <int DIM, int ROW>
-__global__ void __launch_bounds__(PT, SS_TICK_MINB) k_tick_spmv(KArgs a) {
+__global__ void SS_TICK_BOUNDS k_tick_spmv(KArgs a) {
   __shared__ int sph[MAXB_SMEM];
   __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
   __shared__ int sflag, s_any_inner;
