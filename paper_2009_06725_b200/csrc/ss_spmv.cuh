@@ -200,92 +200,13 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
 #endif
 constexpr int ROW_LANES = SS_ROW_LANES;
 
-// SS_ROW_PREFETCH: issue every index and matrix load of a lane's row (node part and pressure part)
-// before any x gather, then all gathers, then the FMAs in the same order -- one dependent load
-// round per row instead of one per loop (same sums, more loads in flight, more registers).
-#ifndef SS_ROW_PREFETCH
-#define SS_ROW_PREFETCH 0
-#endif
-
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
                                                   const double2* __restrict__ x, int gl, double2 (&acc)[DIM],
                                                   int xs = 1) {
 #pragma unroll
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
-#if SS_ROW_PREFETCH
   if (r >= 0) {
-    constexpr int MN = 5, MP = 2;
-    const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-    const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
-    int B[MN], pc[MP];
-    double2 a[MN];
-    double dv[MP][DIM];
-#pragma unroll
-    for (int u = 0; u < MN; ++u) {
-      const int e = e0 + gl + ROW_LANES * u;
-      B[u] = e < e1 ? ldm(op.ncol + e) : -1;
-      a[u] = e < e1 ? ldm(op.sm + e) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < MP; ++u) {
-      const int e = p0 + gl + ROW_LANES * u;
-      pc[u] = e < p1 ? ldm(op.pcol + e) : -1;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) dv[u][d] = e < p1 ? ldm(op.dp + (size_t)e * DIM + d) : 0.0;
-    }
-    double2 xv[MN][DIM], xp[MP];
-#pragma unroll
-    for (int u = 0; u < MN; ++u)
-#pragma unroll
-      for (int d = 0; d < DIM; ++d)
-        xv[u][d] = B[u] >= 0 ? x[((size_t)B[u] * DIM + d) * xs] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < MP; ++u) xp[u] = pc[u] >= 0 ? x[(size_t)(op.nfv + pc[u]) * xs] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < MN; ++u) {
-      if (B[u] < 0) continue;
-      const double am = omega * a[u].y;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        acc[d].x += a[u].x * xv[u][d].x - am * xv[u][d].y;
-        acc[d].y += a[u].x * xv[u][d].y + am * xv[u][d].x;
-      }
-    }
-    for (int e = e0 + gl + ROW_LANES * MN; e < e1; e += ROW_LANES) {   // long rows (rare)
-      const int Bq = ldm(op.ncol + e);
-      const double2 aq = ldm(op.sm + e);
-      const double am = omega * aq.y;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const double2 v = x[((size_t)Bq * DIM + d) * xs];
-        acc[d].x += aq.x * v.x - am * v.y;
-        acc[d].y += aq.x * v.y + am * v.x;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < MP; ++u) {
-      if (pc[u] < 0) continue;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        acc[d].x += dv[u][d] * xp[u].x;
-        acc[d].y += dv[u][d] * xp[u].y;
-      }
-    }
-    for (int e = p0 + gl + ROW_LANES * MP; e < p1; e += ROW_LANES) {
-      const double2 v = x[(size_t)(op.nfv + ldm(op.pcol + e)) * xs];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const double dq = ldm(op.dp + (size_t)e * DIM + d);
-        acc[d].x += dq * v.x;
-        acc[d].y += dq * v.y;
-      }
-    }
-  }
-  if (false) {
-#else
-  if (r >= 0) {
-#endif
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
 #pragma unroll 4
     for (int e = e0 + gl; e < e1; e += ROW_LANES) {
