@@ -356,6 +356,15 @@ class SaddleOperator:
         if ws is None or ws.max_batch < nb or ws.hist_cap < hist_cap:
             if ws is not None:
                 ws.close()
+            torch = _lib.torch_mod()
+            need = self.workspace_bytes(restart, nb, hist_cap)
+            free, _ = torch.cuda.mem_get_info(self.device)
+            if need > free:
+                from .errors import DeviceError
+
+                raise DeviceError(f"Krylov workspace for {nb} mode(s) at restart {restart} needs {need / 2**30:.1f} GiB; "
+                                  f"{free / 2**30:.1f} GiB of device memory is free (fewer modes per batch, a smaller "
+                                  f"restart, or free other workspaces: SaddleOperator.release_workspaces)")
             ws = KrylovWorkspace.for_operator(self, restart, nb, hist_cap)
             self._krylov[key] = ws
         return ws

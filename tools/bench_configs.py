@@ -3,7 +3,7 @@ host setup time (mesh generation + promotion, pattern, assembly, rhs), the modes
 at restart 200, one graphed 200-iteration cycle after a warm-up cycle (GMRES mode-iterations/s),
 and the per-kernel split of an instrumented cycle.
 
-    python tools/bench_configs.py [c3 c4 c5] > profiles/r1_configs.jsonl
+    python tools/bench_configs.py [c3 c4 c5] > profiles/r2_configs.jsonl
 """
 import json
 import os
@@ -20,6 +20,11 @@ from paper_2009_06725_b200.workloads import c3_case, c4_case, c5_case  # noqa: E
 
 RESTART, BUDGET, TOL = 200, 200, 1e-10
 for name in sys.argv[1:] or ["c3", "c4", "c5"]:
+    import gc
+
+    ws = op = b = case = q = None   # release the previous config's workspace and operator
+    gc.collect()
+    torch.cuda.empty_cache()
     t0 = time.perf_counter()
     case = {"c3": c3_case, "c4": c4_case, "c5": c5_case}[name]()
     q = case.qmesh
