@@ -33,7 +33,7 @@ typedef struct ss_comm ss_comm;       /* NCCL communicator for the mode-field ga
 #define SS_COMM_ID_BYTES 128
 
 /* ABI revision: the Python binding refuses (rebuilds) a library whose ss_version() differs. */
-#define SS_ABI_VERSION 4
+#define SS_ABI_VERSION 5
 
 const char* ss_last_error(void);
 int ss_version(void);
@@ -191,6 +191,9 @@ void ss_comm_destroy(ss_comm* c);
 int ss_comm_gather_modes(ss_comm* c, const double* send_dev, int64_t n_local, int64_t count, int64_t ld,
                          double* recv_dev, const int64_t* counts_host, const int64_t* dest_host, int root,
                          void* stream);
+/* In-place sum over ranks of n doubles into the root's buffer (ncclReduce): per-GPU partial
+ * reconstructions sum to u(x, t) on one rank (fused reconstruction + collective). */
+int ss_comm_reduce_sum(ss_comm* c, double* buf_dev, int64_t n, int root, void* stream);
 /* In-place elementwise max over ranks of n doubles on the device. */
 int ss_comm_allreduce_max(ss_comm* c, double* buf_dev, int64_t n, void* stream);
 

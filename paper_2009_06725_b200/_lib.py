@@ -82,12 +82,13 @@ SIGNATURES = {
     "ss_comm_destroy": (None, [P]),
     "ss_comm_gather_modes": (I32, [P, P, I64, I64, I64, P, PI64, PI64, I32, P]),
     "ss_comm_allreduce_max": (I32, [P, P, I64, P]),
+    "ss_comm_reduce_sum": (I32, [P, P, I64, I32, P]),
 }
 
 _lib = None
 
 # Must equal SS_ABI_VERSION in include/spectralstokes_b200.h (bumped whenever an entry point changes).
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 def load(build_if_missing: bool = True):

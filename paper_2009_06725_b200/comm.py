@@ -109,6 +109,15 @@ class ModeComm:
                   _lib.stream_ptr(local.device))
         return out if self.rank == root else None
 
+    def reduce_sum(self, values, root: int = 0):
+        """Sum a float64 device tensor over ranks into ``root``'s copy (in place; ncclReduce)."""
+        if values.dtype.is_complex or values.element_size() != 8:
+            raise ValueError("reduce_sum takes a float64 tensor")
+        values = values.contiguous()
+        _lib.call("ss_comm_reduce_sum", self._h, _lib.dptr(values), values.numel(), int(root),
+                  _lib.stream_ptr(values.device))
+        return values
+
     def allreduce_max(self, values):
         """Elementwise max over ranks of a float64 device tensor (in place)."""
         _lib.call("ss_comm_allreduce_max", self._h, _lib.dptr(values), values.numel(), _lib.stream_ptr(values.device))

@@ -33,6 +33,8 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
   ncclResult_t (*getVersion)(int*) = nullptr;
 };
@@ -67,6 +69,7 @@ int nccl_load() {
   api.send = (decltype(api.send))sym("ncclSend");
   api.recv = (decltype(api.recv))sym("ncclRecv");
   api.allReduce = (decltype(api.allReduce))sym("ncclAllReduce");
+  api.reduce = (decltype(api.reduce))sym("ncclReduce");
   api.errorString = (decltype(api.errorString))sym("ncclGetErrorString");
   api.getVersion = (decltype(api.getVersion))sym("ncclGetVersion");
   if (!ok) {
@@ -195,5 +198,14 @@ extern "C" int ss_comm_allreduce_max(ss_comm* c, double* buf, int64_t n, void* s
   if (!c || (n > 0 && !buf)) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
   SS_CUDA(cudaSetDevice(c->device));
   SS_NCCL(g_nccl.allReduce(buf, buf, (size_t)n, ncclFloat64, ncclMax, c->comm, (cudaStream_t)stream_));
+  return SS_OK;
+}
+
+// Sum of n doubles over ranks into the root's buffer (in place on every rank's send buffer; the
+// root's holds the result): per-GPU partial reconstructions -> the full u(x, t) on one rank.
+extern "C" int ss_comm_reduce_sum(ss_comm* c, double* buf, int64_t n, int root, void* stream_) {
+  if (!c || (n > 0 && !buf) || root < 0 || root >= c->nranks) { ss_set_error("bad arguments"); return SS_ERR_ARG; }
+  SS_CUDA(cudaSetDevice(c->device));
+  SS_NCCL(g_nccl.reduce(buf, buf, (size_t)n, ncclFloat64, ncclSum, root, c->comm, (cudaStream_t)stream_));
   return SS_OK;
 }

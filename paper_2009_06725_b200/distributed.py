@@ -26,7 +26,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["lpt_shard", "expected_iterations", "calibrate_iterations", "iterations_from_first_cycle",
-           "gather_mode_fields", "solve_mode_systems_distributed", "DEFAULT_3D_MODEL"]
+           "gather_mode_fields", "solve_mode_systems_distributed", "reconstruct_distributed", "DEFAULT_3D_MODEL"]
 
 # Iterations to 1e-10 (restart 200) measured on the GPU at BASELINE config 2 (n = 796 978;
 # profiles/r2_c2_converge.json, tools/c2_converge.py): mode 1 336 974, mode 16 886 922 -> per mode-1
@@ -166,3 +166,44 @@ def solve_mode_systems_distributed(qmesh, props, indices, omegas, g_modes, h_mod
     U = full[:, :nu].reshape(-1, qmesh.n_velocity_nodes, qmesh.dim)
     P = full[:, nu:]
     return U, P, [s.report for s in sols], plan
+
+
+def reconstruct_distributed(local_solutions, times, rank: int, world: int, group=None, comm=None, dst: int = 0):
+    """u(x, t_j), p(x, t_j) on rank ``dst`` from modes sharded over ranks, without gathering them:
+    each rank reconstructs its own modes for all samples (``reconstruct_series``, one fused launch)
+    and the partial sums are added over ranks (``ss_comm_reduce_sum``: ncclReduce; gloo ``reduce``
+    in the CPU tests).  Cheaper than gathering the modal fields when the number of samples T is
+    below twice the modes per rank.  Returns ``(U, P)`` (T, n_vn, dim) / (T, n_vert)
+    host arrays on ``dst`` and None elsewhere; a rank with no modes contributes zeros.
+    """
+    import torch
+
+    from .spectral import reconstruct_series
+
+    times = np.atleast_1d(np.asarray(times, dtype=float))
+    if local_solutions:
+        u, p = reconstruct_series(local_solutions, times)
+        shape_u = u.shape[1:]
+        flat = np.concatenate([u.reshape(times.size, -1), p], axis=1)
+    else:
+        flat = None
+    # every rank needs the field sizes: take them from the first rank that has modes
+    if comm is not None:
+        dev = torch.device("cuda", comm.device)
+        buf = torch.from_numpy(flat).to(dev) if flat is not None else None
+        if buf is None:
+            raise ValueError("every rank needs at least one mode for the NCCL reduction (plan with world <= modes)")
+        comm.reduce_sum(buf, root=dst)
+        out = buf.cpu().numpy() if rank == dst else None
+    else:
+        import torch.distributed as dist
+
+        t = torch.from_numpy(flat) if flat is not None else None
+        if t is None:
+            raise ValueError("every rank needs at least one mode (plan with world <= modes)")
+        dist.reduce(t, dst=dst, group=group)
+        out = t.numpy() if rank == dst else None
+    if out is None:
+        return None, None
+    nu = int(np.prod(shape_u))
+    return out[:, :nu].reshape((times.size,) + tuple(shape_u)), out[:, nu:]

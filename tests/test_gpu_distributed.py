@@ -90,3 +90,52 @@ def test_distributed_solve_world2_matches_single_process():
         assert np.array_equal(U[k], s.velocity) and np.array_equal(P[k], s.pressure)
     iters = {plan[r][j]: it for r in (0, 1) for j, it in enumerate(out[r][1])}
     assert [iters[k] for k in range(len(idx))] == [s.report.iterations for s in ref]
+
+
+def test_nccl_reduce_single_rank():
+    from paper_2009_06725_b200.comm import ModeComm
+
+    comm = ModeComm.single(0)
+    t = torch.randn(1000, dtype=torch.float64, device="cuda")
+    ref = t.clone()
+    comm.reduce_sum(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, ref)
+    comm.close()
+
+
+def _recon_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2009_06725_b200 import solve_mode_systems
+        from paper_2009_06725_b200.distributed import expected_iterations, lpt_shard, reconstruct_distributed
+
+        case, props, idx, om, h, settings = _c1_inputs()
+        plan = lpt_shard(expected_iterations(idx, 2), world)
+        mine = plan[rank]
+        sols = solve_mode_systems(case.qmesh, props, [idx[i] for i in mine], om[mine], None, [h[i] for i in mine],
+                                  settings)
+        U, P = reconstruct_distributed(sols, [0.0, 0.3, 0.7], rank, world)
+        out[rank] = None if U is None else (U, P)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reconstruct_distributed_world2_matches_single_process():
+    """Per-rank partial reconstructions summed over ranks (gloo reduce here; ncclReduce through
+    ss_comm_reduce_sum on GPUs) equal the single-process reconstruction to rounding."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_recon_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    from paper_2009_06725_b200 import reconstruct_series, solve_mode_systems
+
+    case, props, idx, om, h, settings = _c1_inputs()
+    sols = solve_mode_systems(case.qmesh, props, idx, om, None, h, settings)
+    Ur, Pr = reconstruct_series(sols, [0.0, 0.3, 0.7])
+    U, P = out[0]
+    assert out[1] is None
+    assert np.abs(U - Ur).max() <= 1e-13 * np.abs(Ur).max()
+    assert np.abs(P - Pr).max() <= 1e-13 * np.abs(Pr).max()
