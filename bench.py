@@ -13,7 +13,7 @@ converged at 1e-10 inside a benchmark, so the rate is GMRES mod
 second.  Measured 3D modes solved/s come from the down-scaled pipes solved to 1e-10 in the same run
 (`c3d_converged`) and the 2D config 1 (`c1_converged`).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c5|c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c5|c4|c3|c2]
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling -- every rank runs one mode-cycle per step
 from its shard, no data-path collective; in the end-to-end leg the solved modal fields of every
@@ -52,6 +52,10 @@ WORKLOADS = {
                modes_per_gpu_per_step=1, slab_layers=9),
     "c2": dict(workload="c2_pipe_199800tets", n_dofs=796978, nnz=32911596, total_modes=17,
                modes_per_gpu_per_step=17, slab_layers=None),
+    "c3": dict(workload="c3_bend_2059200tets", n_dofs=8394503, nnz=354820086, total_modes=64,
+               modes_per_gpu_per_step=6, slab_layers=None),
+    "c4": dict(workload="c4_yjunction_4960116tets", n_dofs=20208154, nnz=854029473, total_modes=32,
+               modes_per_gpu_per_step=2, slab_layers=None),
 }
 
 
@@ -133,9 +137,17 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 
 def _oracle_case(key):
-    from paper_2009_06725_b200.workloads import c2_case, c5_slab
+    """The CPU sample of a workload: config 2 itself; a 9-layer slab of config 5; for configs 3 and 4
+    a down-scaled instance of the same generator (per-DOF work scaled by n, like the slab)."""
+    from paper_2009_06725_b200.workloads import c2_case, c3_case, c4_case, c5_slab
 
-    return c5_slab(WORKLOADS[key]["slab_layers"]) if key == "c5" else c2_case()
+    if key == "c5":
+        return c5_slab(WORKLOADS[key]["slab_layers"])
+    if key == "c3":
+        return c3_case(6)
+    if key == "c4":
+        return c4_case(6)
+    return c2_case()
 
 
 _CACHE = {}
@@ -175,6 +187,9 @@ def _cpu_sample_text(key, det, procs):
     if key == "c5":
         base += (f", a 9-layer slab of config 5 with its cross-section, spacing and jitter), scaled by "
                  f"n_c5/n_slab = {det['scale']:.2f} (per-iteration work is linear in n)")
+    elif key in ("c3", "c4"):
+        base += (f", a down-scaled instance of the config-{key[1]} generator), scaled by n/n_sample = "
+                 f"{det['scale']:.2f} (per-iteration work is linear in n)")
     else:
         base += ")"
     return base + f"; {procs} process(es); per-mode oracle assembly ({det['t_assembly']:.1f} s on the sample) " \
@@ -225,7 +240,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": f"synthetic (seeded, BASELINE config {'5' if args.workload == 'c5' else '2'})",
+        "data": f"synthetic (seeded, BASELINE config {args.workload[1]})",
         "config": config_dict(args.workload),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": _cpu_sample_text(args.workload, det, procs) + "; value = sum over processes of "
@@ -244,9 +259,9 @@ def _setup_workload(key, world, rank):
     from paper_2009_06725_b200 import FluidProps
     from paper_2009_06725_b200.assembly import get_operator
     from paper_2009_06725_b200.distributed import expected_iterations, lpt_shard
-    from paper_2009_06725_b200.workloads import c2_case, c5_case
+    from paper_2009_06725_b200.workloads import c2_case, c3_case, c4_case, c5_case
 
-    case = c5_case() if key == "c5" else c2_case()
+    case = {"c2": c2_case, "c3": c3_case, "c4": c4_case, "c5": c5_case}[key]()
     q = case.qmesh
     props = FluidProps(case.density, case.viscosity)
     op = get_operator(q, props)
@@ -452,7 +467,7 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128",
-            "data": f"synthetic (seeded, BASELINE config {'5' if key == 'c5' else '2'})",
+            "data": f"synthetic (seeded, BASELINE config {key[1]})",
             "config": cfg,
             "setup_s": setup_s,
             "projected_modes_per_s": _projection(key, value),
