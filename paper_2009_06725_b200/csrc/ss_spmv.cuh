@@ -199,6 +199,9 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
 #define SS_ROW_LANES 8
 #endif
 constexpr int ROW_LANES = SS_ROW_LANES;
+#ifndef SS_ROW_UNROLL
+#define SS_ROW_UNROLL 4   // node entries of a lane's row loaded per loop round
+#endif
 
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
@@ -208,7 +211,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
   if (r >= 0) {
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-#pragma unroll 4
+#pragma unroll SS_ROW_UNROLL
     for (int e = e0 + gl; e < e1; e += ROW_LANES) {
       const int B = ldm(op.ncol + e);
       const double2 a = ldm(op.sm + e);
