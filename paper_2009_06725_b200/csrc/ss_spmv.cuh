@@ -200,8 +200,9 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
 #endif
 constexpr int ROW_LANES = SS_ROW_LANES;
 #ifndef SS_ROW_UNROLL
-#define SS_ROW_UNROLL 4   // node entries of a lane's row loaded per loop round
+#define SS_ROW_UNROLL 4
 #endif
+constexpr int ROW_UNROLL = SS_ROW_UNROLL;   // node entries of a lane's row loaded per loop round
 
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
@@ -211,7 +212,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
   if (r >= 0) {
     const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-#pragma unroll SS_ROW_UNROLL
+#pragma unroll ROW_UNROLL
     for (int e = e0 + gl; e < e1; e += ROW_LANES) {
       const int B = ldm(op.ncol + e);
       const double2 a = ldm(op.sm + e);
