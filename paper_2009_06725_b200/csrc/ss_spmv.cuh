@@ -93,6 +93,11 @@ __device__ __forceinline__ double2 ldm(const double2* p) {
 #endif
 }
 
+#ifndef SS_PRES_UNROLL
+#define SS_PRES_UNROLL 1
+#endif
+constexpr int PRES_UNROLL = SS_PRES_UNROLL;   // entries per lane of a pressure row loaded per round
+
 // Jacobi scale of velocity node row r at frequency w: 1/(S'_rr + i w M'_rr), 1 if that is 0
 // (krylov.py:49-60 on the reduced matrix's diagonal; the pressure diagonal is 0 -> 1).
 __device__ __forceinline__ double2 saddle_jacobi(const SsOperatorDev& op, int r, double omega) {
@@ -146,6 +151,7 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
                                                    const double2* __restrict__ x, int lane, int xs = 1) {
   double2 acc = make_double2(0.0, 0.0);
   const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
+#pragma unroll PRES_UNROLL
   for (int e = e0 + lane; e < e1; e += 32) {
     const double2* xb = x + (size_t)ldm(op.tcol + e) * DIM * xs;
 #pragma unroll
