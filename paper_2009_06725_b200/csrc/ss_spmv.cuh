@@ -206,7 +206,7 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
 #endif
 constexpr int ROW_LANES = SS_ROW_LANES;
 #ifndef SS_ROW_UNROLL
-#define SS_ROW_UNROLL 4
+#define SS_ROW_UNROLL 8
 #endif
 constexpr int ROW_UNROLL = SS_ROW_UNROLL;   // node entries of a lane's row loaded per loop round
 
