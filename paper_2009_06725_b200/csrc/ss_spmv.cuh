@@ -307,6 +307,11 @@ __device__ __forceinline__ double2 ldnc2(const double2* p) {
   return v;
 }
 
+#ifndef SS_IL_UNROLL
+#define SS_IL_UNROLL 4
+#endif
+constexpr int IL_U = SS_IL_UNROLL;   // node entries per load round of a (row, mode) thread
+
 // Mode-interleaved batched SpMV over one row block (the GMRES tick's inner SpMV and the
 // standalone ss_spmv_batched_interleaved).  x is [row][ps] (column m = mode m), y is [m][ld].
 // Threads walk the block's (row, mode) pairs, mode fastest: matrix loads are broadcasts and the
@@ -333,18 +338,18 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
       for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
       const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
       int e = e0;
-      for (; e + 4 <= e1; e += 4) {
-        int B[4];
-        double2 sm[4];
+      for (; e + IL_U <= e1; e += IL_U) {
+        int B[IL_U];
+        double2 sm[IL_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { B[u] = __ldg(op.ncol + e + u); sm[u] = __ldg(op.sm + e + u); }
-        double2 v[4][DIM];
+        for (int u = 0; u < IL_U; ++u) { B[u] = __ldg(op.ncol + e + u); sm[u] = __ldg(op.sm + e + u); }
+        double2 v[IL_U][DIM];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < IL_U; ++u)
 #pragma unroll
           for (int d = 0; d < DIM; ++d) v[u][d] = ldnc2(P + ((size_t)B[u] * DIM + d) * ps);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < IL_U; ++u) {
           const double am = om * sm[u].y;
 #pragma unroll
           for (int d = 0; d < DIM; ++d) {
