@@ -216,20 +216,14 @@ __device__ __forceinline__ int4 row_ranges(const SsOperatorDev& op, int r) {
   return make_int4(__ldg(op.nptr + r), __ldg(op.nptr + r + 1), __ldg(op.pptr + r), __ldg(op.pptr + r + 1));
 }
 
-// SS_ROW_PTR_PREFETCH: saddle_block loads the next row's entry ranges before working on the
-// current row (one dependent load round less per row; same sums).
-#ifndef SS_ROW_PTR_PREFETCH
-#define SS_ROW_PTR_PREFETCH 0
-#endif
-
 template <int DIM>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
                                                   const double2* __restrict__ x, int gl, double2 (&acc)[DIM],
-                                                  int xs = 1, int4 rg = make_int4(-1, -1, -1, -1)) {
+                                                  int xs = 1) {
 #pragma unroll
   for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
   if (r >= 0) {
-    if (rg.x < 0) rg = row_ranges(op, r);
+    const int4 rg = row_ranges(op, r);   // node and pressure ranges in one load round
     const int e0 = rg.x, e1 = rg.y;
 #pragma unroll ROW_UNROLL
     for (int e = e0 + gl; e < e1; e += ROW_LANES) {
@@ -276,22 +270,12 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
     const int grp = lane / ROW_LANES, gl = lane % ROW_LANES;
     constexpr int ITERS = SPMV_VROWS / (8 * RPW);
     const int rbase = blk * SPMV_VROWS + warp * RPW + grp;
-#if SS_ROW_PTR_PREFETCH
-    int4 rg = row_ranges(op, rbase < op.nfree ? rbase : -1);
-#endif
 #pragma unroll 1
     for (int it = 0; it < ITERS; ++it) {
       const int r = rbase + it * 8 * RPW;
       const bool ok = r < op.nfree;
       double2 acc[DIM];
-#if SS_ROW_PTR_PREFETCH
-      const int rn = r + 8 * RPW;
-      const int4 rg_next = row_ranges(op, (it + 1 < ITERS && rn < op.nfree) ? rn : -1);
-      saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc, xs, rg);
-      rg = rg_next;
-#else
       saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc, xs);
-#endif
       if (ok && gl < DIM) {
         double2 v = acc[0];
 #pragma unroll
