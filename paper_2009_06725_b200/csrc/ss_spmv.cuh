@@ -210,10 +210,6 @@ constexpr int ROW_LANES = SS_ROW_LANES;
 #endif
 constexpr int ROW_UNROLL = SS_ROW_UNROLL;   // node entries of a lane's row loaded per loop round
 
-#ifndef SS_ROW_PHOIST
-#define SS_ROW_PHOIST 0   // 1: a lane's first pressure entry is loaded (and gathered) before the node loop
-#endif
-
 // Entry ranges of node row r: {nptr[r], nptr[r+1], pptr[r], pptr[r+1]} (empty for r < 0).
 __device__ __forceinline__ int4 row_ranges(const SsOperatorDev& op, int r) {
   if (r < 0) return make_int4(0, 0, 0, 0);
@@ -229,16 +225,6 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
   if (r >= 0) {
     const int4 rg = row_ranges(op, r);   // node and pressure ranges in one load round
     const int e0 = rg.x, e1 = rg.y;
-#if SS_ROW_PHOIST
-    // the lane's first pressure entry: index and coefficients loaded with the node entries
-    const int q0 = rg.z + gl;
-    const bool hq = q0 < rg.w;
-    const int pcq = hq ? ldm(op.pcol + q0) : 0;
-    double dq[DIM];
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) dq[d] = hq ? ldm(op.dp + (size_t)q0 * DIM + d) : 0.0;
-    const double2 vq = hq ? x[(size_t)(op.nfv + pcq) * xs] : make_double2(0.0, 0.0);
-#endif
 #pragma unroll ROW_UNROLL
     for (int e = e0 + gl; e < e1; e += ROW_LANES) {
       const int B = ldm(op.ncol + e);
@@ -253,20 +239,8 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
       }
     }
     const int p0 = rg.z, p1 = rg.w;
-#if SS_ROW_PHOIST
-    if (hq) {
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        acc[d].x += dq[d] * vq.x;
-        acc[d].y += dq[d] * vq.y;
-      }
-    }
-#pragma unroll 2
-    for (int e = p0 + gl + ROW_LANES; e < p1; e += ROW_LANES) {
-#else
 #pragma unroll 2
     for (int e = p0 + gl; e < p1; e += ROW_LANES) {
-#endif
       const double2 v = x[(size_t)(op.nfv + ldm(op.pcol + e)) * xs];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
@@ -342,9 +316,6 @@ __device__ __forceinline__ double2 ldnc2(const double2* p) {
   return v;
 }
 
-#ifndef SS_IL_RANGES
-#define SS_IL_RANGES 0   // 1: the interleaved SpMV loads a row's pressure range with its node range
-#endif
 #ifndef SS_IL_UNROLL
 #define SS_IL_UNROLL 4
 #endif
@@ -375,9 +346,6 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
 #pragma unroll
       for (int d = 0; d < DIM; ++d) acc[d] = make_double2(0.0, 0.0);
       const int e0 = __ldg(op.nptr + r), e1 = __ldg(op.nptr + r + 1);
-#if SS_IL_RANGES
-      const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);   // with the node range
-#endif
       int e = e0;
       for (; e + IL_U <= e1; e += IL_U) {
         int B[IL_U];
@@ -410,9 +378,7 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
           acc[d].y += sm.x * v.y + am * v.x;
         }
       }
-#if !SS_IL_RANGES
       const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
-#endif
 #pragma unroll 4
       for (int q = p0; q < p1; ++q) {
         const double2 v = ldnc2(P + (size_t)(op.nfv + __ldg(op.pcol + q)) * ps);
