@@ -14,10 +14,10 @@ import torch  # noqa: E402
 
 from paper_2009_06725_b200 import FluidProps  # noqa: E402
 from paper_2009_06725_b200.assembly import assemble_mode_systems, get_operator  # noqa: E402
-from paper_2009_06725_b200.workloads import c2_case, c3_case, c5_case, pipe3d_case  # noqa: E402
+from paper_2009_06725_b200.workloads import c2_case, c3_case, c4_case, c5_case, pipe3d_case  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-case = {"c2": c2_case, "c3": c3_case, "c5": c5_case, "pipe3d": pipe3d_case}[name]()
+case = {"c2": c2_case, "c3": c3_case, "c4": c4_case, "c5": c5_case, "pipe3d": pipe3d_case}[name]()
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else (1 if name == "c5" else case.n_modes + 1)
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 q = case.qmesh
