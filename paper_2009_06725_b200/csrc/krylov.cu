@@ -1133,14 +1133,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   int rc;
   if ((rc = kalloc(K, B * a.jcap * a.ld, &a.Q))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.W))) return rc;
-  // mode-interleaved P[row][pstride]: optionally pad the row stride to a multiple of
-  // SS_PSTRIDE_ALIGN modes so every row's run of modes starts on a 128-byte line (8 modes)
+  if ((rc = kalloc(K, B * a.ld, &a.P))) return rc;
   a.pstride = max_batch;
-  if (const char* e = getenv("SS_PSTRIDE_ALIGN")) {
-    const int al = std::max(1, atoi(e));
-    if (max_batch > 1) a.pstride = (int)ss_round_up(max_batch, al);
-  }
-  if ((rc = kalloc(K, (size_t)a.pstride * a.ld, &a.P))) return rc;
   if (a.spmv_split < 1) a.spmv_split = 1;   // the saddle creator sets it from nsb
   if ((rc = kalloc(K, B * a.ld, &a.X))) return rc;
   if ((rc = kalloc(K, B * a.ld, &a.RHS))) return rc;
