@@ -14,6 +14,9 @@ SOURCES = ["pattern.cpp", "assemble.cu", "krylov.cu", "reconstruct.cu", "snapsho
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
+    # no implicit FMA contraction: sums round the same in every kernel they are inlined into
+    # (hot loops use explicit __fma_rn, ss_spmv.cuh cfma/rfma)
+    "-fmad=false",
     "-Xcompiler", "-fPIC,-fopenmp,-O3",
     "-Xptxas", "-v",
     f"-I{PKG.parent / 'include'}",

@@ -32,6 +32,9 @@
 #include "ss_pattern.h"
 #include "ss_spmv.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 enum Phase : int { PH_IDLE = 0, PH_RESID = 1, PH_START = 2, PH_INNER = 3, PH_XUPDATE = 4, PH_DONE = 5 };
 
 struct ModeCtl {
@@ -80,7 +83,10 @@ struct KArgs {
   int row_spmv;                // tick SpMV: per-mode 8-lanes-per-row blocks (n >= SS_ROW_SPMV_N) instead of interleaved
   int wide;                    // restart > WIDE_RESTART: basis passes without the shared-memory ring (any J)
   int stream_spmv;             // row layout: TMA-staged persistent SpMV (1) or one CTA per row block (0)
+  int fused;                   // running inside k_tick_fused (persistent, grid barriers between phases)
+  long long* ptime;            // fused-kernel phase timestamps [tick % FUSED_PROF_TICKS][5] (SS_FUSED_PROF)
 };
+constexpr int FUSED_PROF_TICKS = 1 << 16;
 
 constexpr int RB = 32;         // rows per block of the row-block-major basis layout
 
@@ -197,17 +203,17 @@ __global__ void __launch_bounds__(PT) k_init(KArgs a) {
 // ------------------------------------------------------------------------------------------------
 constexpr int MAXB_SMEM = 256;   // modes whose per-tick state is cached in shared memory
 
-template <int DIM>
-__device__ __forceinline__ void spmv_inner_interleaved(const KArgs& a, int blk, const int* sph,
+template <int DIM, bool NC>
+__device__ __forceinline__ void spmv_inner_interleaved(const KArgs& a, int blk, int sub, const int* sph,
                                                        const double* som, const double* sxs) {
-  saddle_block_interleaved<DIM>(
-      a.op, blk, blockIdx.x % a.spmv_split, a.spmv_split, a.nb, a.pstride, a.P, a.W, a.ld, a.jacobi,
+  saddle_block_interleaved<DIM, NC>(
+      a.op, blk, sub, a.spmv_split, a.nb, a.pstride, a.P, a.W, a.ld, a.jacobi,
       [&](int m) { return sph[m] == PH_INNER || sph[m] == PH_START; },
       [&](int m) { return som[m]; }, [&](int m) { return sxs[m]; });
 }
 
 // RESID for one mode (row layout X): t = b - A x, r = s.t -> P (interleaved) and Q[0]; norms.
-template <int DIM>
+template <int DIM, bool NC = true>
 __device__ __forceinline__ void spmv_resid_mode(const KArgs& a, int b, int sb, double om) {
   __shared__ double red[2][PT / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -223,8 +229,8 @@ __device__ __forceinline__ void spmv_resid_mode(const KArgs& a, int b, int sb, d
     tt += cabs2(t);
     rr += cabs2(r);
   };
-  if (a.kind == 0) saddle_block<DIM>(a.op, sb, om, x, emit);
-  else csr_block(a.csr, a.csr.nvals > 1 ? b : 0, sb, x, emit);
+  if (a.kind == 0) saddle_block<DIM, NC>(a.op, sb, om, x, emit);
+  else csr_block<NC>(a.csr, a.csr.nvals > 1 ? b : 0, sb, x, emit);
   tt = warp_sum(tt);
   rr = warp_sum(rr);
   if (lane == 0) { red[0][warp] = tt; red[1][warp] = rr; }
@@ -250,8 +256,7 @@ __device__ __forceinline__ void spmv_inner_csr_mode(const KArgs& a, int b, int s
     for (int e = A.indptr[row] + lane; e < A.indptr[row + 1]; e += 32) {
       const double2 av = vals[e];
       const double2 v = a.P[(size_t)A.indices[e] * a.pstride + b];
-      acc.x += av.x * v.x - av.y * v.y;
-      acc.y += av.x * v.y + av.y * v.x;
+      acc = cfma(av, v, acc);
     }
     acc.x = warp_sum(acc.x);
     acc.y = warp_sum(acc.y);
@@ -264,14 +269,13 @@ __device__ __forceinline__ void spmv_inner_csr_mode(const KArgs& a, int b, int s
 
 // Cycle-boundary decisions of mode b once every CTA has contributed (krylov.py:93-103,155-162).
 // Called by the last CTA of the tick SpMV for every mode it touched.
-__device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int phase) {
+__device__ __forceinline__ void spmv_finalize_mode(const KArgs& a, int b, int phase, double2* rsum) {
   ModeCtl* c = a.ctl + b;
   if (phase != PH_RESID) {
     if (threadIdx.x == 0 && phase == PH_START) c->phase = PH_INNER;
     __syncthreads();
     return;
   }
-  __shared__ double2 rsum[PT];
   double2 acc = make_double2(0.0, 0.0);
   for (int q = threadIdx.x; q < a.nsb; q += PT) {
     const double2 v = __ldcg(a.spart + (size_t)b * a.nsb + q);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
   __shared__ int sph[MAXB_SMEM];
   __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
   __shared__ int sflag, s_any_inner;
+  __shared__ double2 rsum[PT];
   extern __shared__ __align__(128) unsigned char sring[];
   __shared__ __align__(8) uint64_t sbar[STREAM_STAGES];
   if (threadIdx.x == 0) s_any_inner = 0;
@@ -358,7 +363,68 @@ __global__ void __launch_bounds__(PT, 2) k_tick_spmv_stream(KArgs a) {
   if (threadIdx.x == 0) a.loop[2] += 1;   // one tick done (per-mode completion ticks, ss_krylov_done_ticks)
   for (int b = 0; b < a.nb; ++b) {
     const int ph = sph[b];
-    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
+    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph, rsum);
+  }
+}
+
+// Tick SpMV over virtual block vb of nvb (a kernel launch: blockIdx.x of gridDim.x; the fused
+// persistent kernel: its CTAs walk the virtual blocks).  Shared state is passed in so that the
+// fused kernel declares it once.
+template <int DIM, int ROW, bool NC>
+__device__ __forceinline__ void tick_spmv_body(const KArgs& a, int vb, int nvb, int* sph, double* som, double* sxs,
+                                               int* sflag, int* s_any_inner, double2* rsum) {
+  const int sb = vb / a.spmv_split, sub = vb % a.spmv_split;
+  if (a.fused) __syncthreads();   // shared state of the previous virtual block
+  if (threadIdx.x == 0) *s_any_inner = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.nb; b += PT) {
+    const ModeCtl* c = a.ctl + b;
+    const int ph = c->phase;
+    sph[b] = ph;
+    som[b] = c->omega;
+    sxs[b] = (ph == PH_INNER || ph == PH_START) ? a.qs[b * a.jcap + c->k] : 0.0;
+    if (ph == PH_INNER || ph == PH_START) *s_any_inner = 1;
+  }
+  __syncthreads();
+  if (ROW) {
+    // very large n (rule on n only, so per-mode results stay batch-invariant; at most a few modes
+    // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
+    // the mode's column of P with stride pstride.  Grid-stride over the row blocks (a few CTAs per
+    // SM): the mode-state prologue and the last-CTA election are paid per CTA, not per block.
+    const int b0 = vb, b1 = a.nsb, bstep = nvb;   // blocks dealt round-robin (measured best)
+    for (int blk = b0; blk < b1; blk += bstep) {
+      if (*s_any_inner)
+        for (int b = 0; b < a.nb; ++b) {
+          if (sph[b] != PH_INNER && sph[b] != PH_START) continue;
+          const double om = som[b], xs = sxs[b];
+          double2* w = a.W + (size_t)b * a.ld;
+          saddle_block<DIM, NC>(a.op, blk, om, a.P + b, [&](int row, double2 v) {
+            const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
+            w[row] = cmul(s, cscale(v, xs));
+          }, a.pstride);
+        }
+      for (int b = 0; b < a.nb; ++b)
+        if (sph[b] == PH_RESID) spmv_resid_mode<DIM, NC>(a, b, blk, som[b]);
+    }
+  } else if (*s_any_inner) {
+    if (a.kind == 0) {
+      spmv_inner_interleaved<DIM, NC>(a, sb, sub, sph, som, sxs);
+    } else {
+      if (sub == 0)
+        for (int b = 0; b < a.nb; ++b)
+          if (sph[b] == PH_INNER || sph[b] == PH_START) spmv_inner_csr_mode(a, b, sb, sxs[b]);
+    }
+  }
+  if (!ROW && sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
+    for (int b = 0; b < a.nb; ++b)
+      if (sph[b] == PH_RESID) spmv_resid_mode<DIM, NC>(a, b, sb, som[b]);
+  // one election for the whole batch (slot 6 of mode 0's counters): the last CTA to finish makes
+  // every mode's cycle decisions
+  if (!last_cta(a, 0, 6, nvb, sflag)) return;
+  if (threadIdx.x == 0) a.loop[2] += 1;   // one tick done (per-mode completion ticks, ss_krylov_done_ticks)
+  for (int b = 0; b < a.nb; ++b) {
+    const int ph = sph[b];
+    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph, rsum);
   }
 }
 
@@ -377,58 +443,8 @@ __global__ void SS_TICK_BOUNDS k_tick_spmv(KArgs a) {
   __shared__ int sph[MAXB_SMEM];
   __shared__ double som[MAXB_SMEM], sxs[MAXB_SMEM];
   __shared__ int sflag, s_any_inner;
-  const int sb = blockIdx.x / a.spmv_split, sub = blockIdx.x % a.spmv_split;
-  if (threadIdx.x == 0) s_any_inner = 0;
-  __syncthreads();
-  for (int b = threadIdx.x; b < a.nb; b += PT) {
-    const ModeCtl* c = a.ctl + b;
-    const int ph = c->phase;
-    sph[b] = ph;
-    som[b] = c->omega;
-    sxs[b] = (ph == PH_INNER || ph == PH_START) ? a.qs[b * a.jcap + c->k] : 0.0;
-    if (ph == PH_INNER || ph == PH_START) s_any_inner = 1;
-  }
-  __syncthreads();
-  if (ROW) {
-    // very large n (rule on n only, so per-mode results stay batch-invariant; at most a few modes
-    // fit a GPU there): 8 lanes per node row with a warp reduction, one mode at a time, reading
-    // the mode's column of P with stride pstride.  Grid-stride over the row blocks (a few CTAs per
-    // SM): the mode-state prologue and the last-CTA election are paid per CTA, not per block.
-    const int b0 = blockIdx.x, b1 = a.nsb, bstep = gridDim.x;   // blocks dealt round-robin (measured best)
-    for (int blk = b0; blk < b1; blk += bstep) {
-      if (s_any_inner)
-        for (int b = 0; b < a.nb; ++b) {
-          if (sph[b] != PH_INNER && sph[b] != PH_START) continue;
-          const double om = som[b], xs = sxs[b];
-          double2* w = a.W + (size_t)b * a.ld;
-          saddle_block<DIM>(a.op, blk, om, a.P + b, [&](int row, double2 v) {
-            const double2 s = row < a.op.nfv && a.jacobi ? saddle_jacobi(a.op, row / DIM, om) : make_double2(1.0, 0.0);
-            w[row] = cmul(s, cscale(v, xs));
-          }, a.pstride);
-        }
-      for (int b = 0; b < a.nb; ++b)
-        if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, blk, som[b]);
-    }
-  } else if (s_any_inner) {
-    if (a.kind == 0) {
-      if (!ROW) spmv_inner_interleaved<DIM>(a, sb, sph, som, sxs);
-    } else {
-      if (sub == 0)
-        for (int b = 0; b < a.nb; ++b)
-          if (sph[b] == PH_INNER || sph[b] == PH_START) spmv_inner_csr_mode(a, b, sb, sxs[b]);
-    }
-  }
-  if (!ROW && sub == 0)   // residual rows of the block are owned by its first sub-CTA (fixed reduction tree)
-    for (int b = 0; b < a.nb; ++b)
-      if (sph[b] == PH_RESID) spmv_resid_mode<DIM>(a, b, sb, som[b]);
-  // one election for the whole batch (slot 6 of mode 0's counters): the last CTA to finish makes
-  // every mode's cycle decisions
-  if (!last_cta(a, 0, 6, (int)gridDim.x, &sflag)) return;
-  if (threadIdx.x == 0) a.loop[2] += 1;   // one tick done (per-mode completion ticks, ss_krylov_done_ticks)
-  for (int b = 0; b < a.nb; ++b) {
-    const int ph = sph[b];
-    if (ph == PH_INNER || ph == PH_START || ph == PH_RESID) spmv_finalize_mode(a, b, ph);
-  }
+  __shared__ double2 rsum[PT];
+  tick_spmv_body<DIM, ROW, true>(a, blockIdx.x, gridDim.x, sph, som, sxs, &sflag, &s_any_inner, rsum);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -501,8 +517,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
         if (j < J) {
           qv[t] = S[j * RB];
           const double2 cf = coef[j];
-          p.x += qv[t].x * cf.x - qv[t].y * cf.y;
-          p.y += qv[t].x * cf.y + qv[t].y * cf.x;
+          p = cfma(qv[t], cf, p);
         } else {
           qv[t] = make_double2(0.0, 0.0);
         }
@@ -521,8 +536,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
       const double2 v = Vb[lane];
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        acc[t].x += qv[t].x * v.x + qv[t].y * v.y;
-        acc[t].y += qv[t].x * v.y - qv[t].y * v.x;
+        acc[t] = cfmaconj(qv[t], v, acc[t]);
       }
     } else if (PASS != PASS_A) {
       for (int cr = 0; cr < nc; cr += 8) {
@@ -535,8 +549,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
 #pragma unroll 4
           for (int j = sl; j < J; j += SL) {
             const double2 q = S[j * RB], cf = coef[j];
-            p.x += q.x * cf.x - q.y * cf.y;
-            p.y += q.x * cf.y + q.y * cf.x;
+            p = cfma(q, cf, p);
           }
         }
         red[tid] = p;
@@ -568,8 +581,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
           const int j = warp + 8 * t;
           if (j < J) {
             const double2 q = S[j * RB];
-            acc[t].x += q.x * v.x + q.y * v.y;
-            acc[t].y += q.x * v.y - q.y * v.x;
+            acc[t] = cfmaconj(q, v, acc[t]);
           }
         }
       }
@@ -577,6 +589,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
     fence_proxy_async();   // generic-proxy smem writes before the async proxy refills this stage
     __syncthreads();
   }
+  if (a.fused && tid < PASS_MAX_STAGES) mbar_inval(&mbar[tid]);   // re-initialised by the next work item
   if (tid == 0 && blk_begin * RB < a.n) {
     // algorithmic bytes of this CTA: J basis rows read + vector read (+ vector/basis row written)
     const int64_t real_rows = min((int64_t)blk_end * RB, (int64_t)a.n) - (int64_t)blk_begin * RB;
@@ -624,8 +637,7 @@ __device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s
       for (int j = warp; j < J; j += PT / 32) {
         const double2 q = S[(size_t)j * RB];
         const double2 cf = PASS == PASS_X ? cc[j] : cscale(cc[j], qs[j]);
-        p.x += q.x * cf.x - q.y * cf.y;
-        p.y += q.x * cf.y + q.y * cf.x;
+        p = cfma(q, cf, p);
       }
       red[tid] = p;
       __syncthreads();
@@ -659,8 +671,7 @@ __device__ __forceinline__ void stream_segment_wide(const KArgs& a, int b, int s
           const int j = j0 + warp + 8 * t;
           if (j < J) {
             const double2 q = S[(size_t)j * RB];
-            acc[t].x += q.x * v.x + q.y * v.y;
-            acc[t].y += q.x * v.y - q.y * v.x;
+            acc[t] = cfmaconj(q, v, acc[t]);
           }
         }
       }
@@ -752,8 +763,7 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
         if (j < J) {
           qv[t] = S[j * RB];
           const double2 cf = coef[j];
-          p.x += qv[t].x * cf.x - qv[t].y * cf.y;
-          p.y += qv[t].x * cf.y + qv[t].y * cf.x;
+          p = cfma(qv[t], cf, p);
         } else {
           qv[t] = make_double2(0.0, 0.0);
         }
@@ -780,14 +790,14 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
       }
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        acc[t].x += qv[t].x * v.x + qv[t].y * v.y;
-        acc[t].y += qv[t].x * v.y - qv[t].y * v.x;
+        acc[t] = cfmaconj(qv[t], v, acc[t]);
       }
       ++bi;
     }
     fence_proxy_async();
     __syncthreads();
   }
+  if (a.fused && tid < PASS_MAX_STAGES) mbar_inval(&mbar[tid]);   // re-initialised by the next work item
   if (tid == 0 && blk_begin * RB < a.n) {
     const int64_t real_rows = min((int64_t)blk_end * RB, (int64_t)a.n) - (int64_t)blk_begin * RB;
     atomicAdd(a.bytes + PASS_B, (unsigned long long)((J + 2) * real_rows * 16));
@@ -808,14 +818,20 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
   }
 }
 
+// One (mode, segment) work item vb of a basis pass (a kernel launch: blockIdx.x; the fused
+// persistent kernel: its CTAs walk the work items).  Shared buffers are passed in (the fused kernel
+// declares them once); coef doubles as the back-substitution vector y of pass C.
 template <int PASS>
-__global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
-  extern __shared__ __align__(128) double2 smem[];
-  __shared__ double2 coef[256];
-  __shared__ double2 red[PASS == PASS_B ? 2 * PT : PT];
-  __shared__ __align__(8) uint64_t mbar[PASS_MAX_STAGES];
-  __shared__ int sflag;
-  const int b = blockIdx.x % a.nb, s = blockIdx.x / a.nb;
+__device__ __forceinline__ void pass_body(const KArgs& a, int vb, double2* smem, double2* coef, double2* red,
+                                          uint64_t* mbar, int* sflag_, int* s_solve_) {
+  int& sflag = *sflag_;
+  int& s_solve = *s_solve_;
+  double2* ys = coef;
+  if (a.fused) {                  // shared buffers of the previous work item / phase
+    fence_proxy_async();          // generic smem writes (pass C staging) before the next bulk copies
+    __syncthreads();
+  }
+  const int b = vb % a.nb, s = vb / a.nb;
   ModeCtl* c = a.ctl + b;
   const int phase = c->phase;
   const int tid = threadIdx.x;
@@ -921,8 +937,6 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   if (PASS == PASS_A || PASS == PASS_B) return;
   // PASS_C: Givens update (krylov.py:115-149).  The H column and the stored rotations are staged
   // in (now idle) shared memory by all threads; one thread runs the serial recurrence on them.
-  __shared__ double2 ys[256];
-  __shared__ int s_solve;
   const int jc = a.jcap;
   // wide restart: the column, rotations and y live in global memory (H column k, CS, SN, Y)
   double2* hcol = a.H + ((size_t)b * a.restart + k) * jc;      // column k, rows 0..restart
@@ -1023,6 +1037,76 @@ __global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
   if (tid == 0) c->phase = PH_XUPDATE;
 }
 
+template <int PASS>
+__global__ void __launch_bounds__(PT, 1) k_pass(KArgs a) {
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ double2 coef[256];
+  __shared__ double2 red[PASS == PASS_B ? 2 * PT : PT];
+  __shared__ __align__(8) uint64_t mbar[PASS_MAX_STAGES];
+  __shared__ int sflag, s_solve;
+  pass_body<PASS>(a, blockIdx.x, smem, coef, red, mbar, &sflag, &s_solve);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Persistent fused tick (small n): ONE cooperative launch runs `nticks` ticks; its CTAs (one per
+// SM) walk the virtual blocks of the tick SpMV and the (mode, segment) work items of passes A, B, C
+// with a grid barrier between phases -- the same work decomposition, reduction trees and last-CTA
+// state changes as the four-kernel tick, so per-mode results are bitwise identical to it, without
+// four kernel launches, four ring fills from a cold start and four launch tails per tick.
+// Memory ordering across phases: the barrier is a gpu-scope fence + arrive/wait (cooperative
+// groups); generic-proxy global writes (W, Q, P, X) are ordered before the next phase's bulk copies
+// by fence.proxy.async on both sides; x-type vectors written in the launch are never read through
+// the non-coherent path (NC = false).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void fused_sync(cg::grid_group& grid) {
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+  grid.sync();
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(PT, 1) k_tick_fused(KArgs a, int nticks, int tick0) {
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ double2 coef[256];
+  __shared__ double2 red[2 * PT];
+  __shared__ __align__(8) uint64_t mbar[PASS_MAX_STAGES];
+  __shared__ int sph[MAXB_SMEM];
+  __shared__ int sflag, s_any, s_solve;
+  // SpMV-phase mode state lives in the upper half of red (the finalize reduction uses the lower
+  // half), so the basis-pass ring keeps the four-kernel tick's size: same chunking, same sums
+  double* som = (double*)(red + PT);
+  double* sxs = som + MAXB_SMEM;
+  cg::grid_group grid = cg::this_grid();
+  const int nspmv = a.nsb * a.spmv_split, npass = a.nb * a.nseg;
+  auto stamp = [&](int t, int q) {   // optional phase timestamps (SS_FUSED_PROF)
+    if (a.ptime && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      a.ptime[(size_t)(t % FUSED_PROF_TICKS) * 5 + q] = (long long)g;
+    }
+  };
+  for (int t = 0; t < nticks; ++t) {
+    const int tt = tick0 + t;
+    stamp(tt, 0);
+    for (int vb = blockIdx.x; vb < nspmv; vb += gridDim.x)
+      tick_spmv_body<DIM, 0, false>(a, vb, nspmv, sph, som, sxs, &sflag, &s_any, red);
+    fused_sync(grid);
+    stamp(tt, 1);
+    // n_done only changes in the SpMV phase: every CTA reads the same value here
+    const bool stop = *(volatile int*)a.n_done >= a.nb;
+    for (int vb = blockIdx.x; vb < npass; vb += gridDim.x) pass_body<PASS_A>(a, vb, smem, coef, red, mbar, &sflag, &s_solve);
+    fused_sync(grid);
+    stamp(tt, 2);
+    for (int vb = blockIdx.x; vb < npass; vb += gridDim.x) pass_body<PASS_B>(a, vb, smem, coef, red, mbar, &sflag, &s_solve);
+    fused_sync(grid);
+    stamp(tt, 3);
+    for (int vb = blockIdx.x; vb < npass; vb += gridDim.x) pass_body<PASS_C>(a, vb, smem, coef, red, mbar, &sflag, &s_solve);
+    fused_sync(grid);
+    stamp(tt, 4);
+    if (stop) break;
+  }
+}
+
 __global__ void k_finalize(KArgs a) {
   const int b = blockIdx.y;
   if (b >= a.nb || !a.ctl[b].zero_x) return;
@@ -1090,6 +1174,10 @@ struct ss_krylov {
   double2* csr_vals_owned = nullptr;
   int stream_ctas = 2 * 148;   // persistent CTAs of the staged tick SpMV (2 per SM)
   int row_ctas = 16 * 148;     // grid-stride CTAs of the row-layout tick SpMV
+  int fused = 0;               // persistent fused tick kernel (option "fused"; default for small n)
+  int fused_grid = 0;          // its CTAs (one per SM), 0 = not set up yet, -1 = unavailable
+  int fused_elems = 0;         // its basis-pass ring (double2 elements)
+  long long* ptime = nullptr;  // fused phase timestamps (SS_FUSED_PROF=path: written per solve)
 };
 
 template <class T>
@@ -1183,6 +1271,13 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
     if (const char* e = getenv("SS_SPMV_STREAM")) K->a.stream_spmv = atoi(e);
   }
   K->ticks_per_graph = n < 200000 ? 16 : 2;
+  // persistent fused tick for small systems, where the four tick kernels are launch/latency bound
+  K->fused = 0;
+  if (const char* e = getenv("SS_FUSED")) K->fused = atoi(e);
+  if (getenv("SS_FUSED_PROF")) {
+    int rc2 = kalloc(K, (size_t)FUSED_PROF_TICKS * 5, &K->ptime);
+    if (rc2) return rc2;
+  }
   if (const char* e = getenv("SS_DEVICE_LOOP")) K->device_loop = atoi(e);
   K->a.x_in_a = 1;
   K->a.gthr[0] = 16;
@@ -1297,6 +1392,8 @@ extern "C" int ss_krylov_set_option(ss_krylov* K, const char* name, int64_t valu
   } else if (opt == "ticks_per_graph") {
     if (value < 1 || value > 1024) { ss_set_error("ticks_per_graph must lie in [1, 1024]"); return SS_ERR_ARG; }
     K->ticks_per_graph = (int)value;
+  } else if (opt == "fused") {
+    K->fused = value ? 1 : 0;
   } else {
     ss_set_error("unknown workspace option '" + opt + "'");
     return SS_ERR_ARG;
@@ -1314,6 +1411,8 @@ extern "C" int ss_krylov_get_option(const ss_krylov* K, const char* name, int64_
   else if (opt == "stream_spmv") *value = K->a.stream_spmv;
   else if (opt == "device_loop") *value = K->device_loop;
   else if (opt == "ticks_per_graph") *value = K->ticks_per_graph;
+  else if (opt == "fused") *value = K->fused;
+  else if (opt == "fused_active") *value = K->fused && !(K->a.kind == 0 && K->a.row_spmv) && K->fused_grid >= 0;
   else { ss_set_error("unknown workspace option '" + opt + "'"); return SS_ERR_ARG; }
   return SS_OK;
 }
@@ -1446,6 +1545,51 @@ static int get_graph(ss_krylov* K, int nb, int jacobi, cudaGraphExec_t* out) {
   return SS_OK;
 }
 
+// Persistent fused tick: shared-memory budget and grid (one CTA per SM) on first use.  The ring
+// shrinks to what the static shared state leaves of the 227 KB per CTA (chunking does not change
+// any sum).  Returns false when the fused kernel cannot run this workspace.
+template <int DIM>
+static bool fused_setup(ss_krylov* K) {
+  if (K->fused_grid != 0) return K->fused_grid > 0;
+  K->fused_grid = -1;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, (const void*)k_tick_fused<DIM>) != cudaSuccess) { cudaGetLastError(); return false; }
+  const int dyn_max = 227 * 1024 - (int)fa.sharedSizeBytes;
+  // the ring must equal the four-kernel tick's (pass C/X chunking sets their slice sums)
+  const int elems = K->a.smem_elems;
+  if (elems > dyn_max / (int)sizeof(double2)) return false;
+  if (cudaFuncSetAttribute((const void*)k_tick_fused<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           elems * (int)sizeof(double2)) != cudaSuccess) { cudaGetLastError(); return false; }
+  int dev = 0, sms = 0, coop = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tick_fused<DIM>, PT,
+                                                            (size_t)elems * sizeof(double2)) != cudaSuccess ||
+      per_sm < 1) { cudaGetLastError(); return false; }
+  K->fused_elems = elems;
+  K->fused_grid = sms;
+  return true;
+}
+
+static bool fused_usable(ss_krylov* K) {
+  if (!K->fused || (K->a.kind == 0 && K->a.row_spmv)) return false;
+  return tick_dim(K) == 3 ? fused_setup<3>(K) : fused_setup<2>(K);
+}
+
+static int launch_fused(ss_krylov* K, const KArgs& a0, int nticks, int tick0, cudaStream_t st) {
+  KArgs a = a0;
+  a.fused = 1;
+  a.x_in_a = 1;
+  a.smem_elems = K->fused_elems;
+  a.ptime = K->ptime;
+  void* args[] = {(void*)&a, (void*)&nticks, (void*)&tick0};
+  const void* f = tick_dim(K) == 3 ? (const void*)k_tick_fused<3> : (const void*)k_tick_fused<2>;
+  SS_CUDA(cudaLaunchCooperativeKernel(f, dim3(K->fused_grid), dim3(PT), args,
+                                      (size_t)K->fused_elems * sizeof(double2), st));
+  return SS_OK;
+}
+
 // Solve nb modes.  rhs/x0 are read from the engine's own RHS/X buffers (see ss_krylov_buffers)
 // when rhs_dev / x_dev are null, otherwise copied in (device pointers, leading dimension ld_in).
 // On return X holds the solutions (also copied to x_dev when given).
@@ -1491,13 +1635,14 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
   // tick bound: every mode finishes within maxiter inner ticks + 2 ticks per cycle
   const int64_t max_ticks = maxiter + 3 * (maxiter / std::max<int64_t>(1, std::min<int64_t>(a.restart, maxiter + 1)) + 2) + 16;
   int64_t ticks = 0;
-  cudaGraphExec_t g;
+  cudaGraphExec_t g = nullptr;
   int rc = SS_OK;
-  if (K->device_loop) {
+  const bool fused = fused_usable(K);
+  if (K->device_loop && !fused) {
     rc = get_while_graph(K, nb, jacobi, &g);
     if (rc) K->device_loop = 0;   // fall back to the host-polled loop
   }
-  if (K->device_loop) {
+  if (K->device_loop && !fused) {
     long long lp[2] = {0, (long long)max_ticks + 2 * K->ticks_per_graph};
     SS_CUDA(cudaMemcpyAsync(a.loop, lp, sizeof(lp), cudaMemcpyHostToDevice, st));
     SS_CUDA(cudaGraphLaunch(g, st));
@@ -1512,13 +1657,17 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
       return SS_ERR_STATE;
     }
   }
-  rc = K->device_loop ? SS_OK : get_graph(K, nb, jacobi, &g);
+  rc = (K->device_loop && !fused) || fused ? SS_OK : get_graph(K, nb, jacobi, &g);
   if (rc) return rc;
-  const int per_graph_launches = (a.x_in_a ? 4 : 5) * K->ticks_per_graph;
+  const int per_graph_launches = fused ? 1 : (a.x_in_a ? 4 : 5) * K->ticks_per_graph;
   int it = 0;
-  bool finished = K->device_loop != 0;
+  bool finished = K->device_loop != 0 && !fused;
   while (!finished) {
-    SS_CUDA(cudaGraphLaunch(g, st));
+    if (fused) {
+      if ((rc = launch_fused(K, a, K->ticks_per_graph, (int)ticks, st))) return rc;
+    } else {
+      SS_CUDA(cudaGraphLaunch(g, st));
+    }
     ss_count_launch(per_graph_launches);
     ticks += K->ticks_per_graph;
     SS_CUDA(cudaMemcpyAsync(K->h_done + (it & 1), a.n_done, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1543,6 +1692,20 @@ extern "C" int ss_krylov_solve(ss_krylov* K, int nb, const double* omegas_host, 
   SS_CUDA(cudaStreamSynchronize(st));
   K->last_ticks = ticks;
   K->last_launches = ss_launch_counter() - launches0;
+  if (fused && K->ptime) {   // per-tick phase durations (us): spmv, A, B, C
+    const int64_t nt = std::min<int64_t>(ticks, FUSED_PROF_TICKS);
+    std::vector<long long> h((size_t)nt * 5);
+    SS_CUDA(cudaMemcpy(h.data(), K->ptime, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(getenv("SS_FUSED_PROF"), "w")) {
+      for (int64_t t = 0; t < nt; ++t) {
+        const long long* r = h.data() + t * 5;
+        if (r[4] <= r[0]) break;
+        fprintf(f, "%.3f,%.3f,%.3f,%.3f\n", 1e-3 * (r[1] - r[0]), 1e-3 * (r[2] - r[1]), 1e-3 * (r[3] - r[2]),
+                1e-3 * (r[4] - r[3]));
+      }
+      fclose(f);
+    }
+  }
   for (int b = 0; b < nb; ++b) {
     if (out_int) {
       out_int[b * 6 + 0] = ctl[b].iters;

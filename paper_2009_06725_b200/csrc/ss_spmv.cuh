@@ -16,6 +16,23 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 __device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 
+// Accumulations with pinned rounding.  The CUDA sources are compiled with -fmad=false, so no
+// expression is contracted implicitly (the result of a sum never depends on the kernel it is
+// inlined into -- the fused tick and the four-kernel tick round identically); the hot loops use
+// these explicit FMAs instead.
+// acc + a*b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  return make_double2(__fma_rn(a.x, b.x, __fma_rn(-a.y, b.y, acc.x)), __fma_rn(a.x, b.y, __fma_rn(a.y, b.x, acc.y)));
+}
+// acc + conj(a)*b
+__device__ __forceinline__ double2 cfmaconj(double2 a, double2 b, double2 acc) {
+  return make_double2(__fma_rn(a.x, b.x, __fma_rn(a.y, b.y, acc.x)), __fma_rn(a.x, b.y, __fma_rn(-a.y, b.x, acc.y)));
+}
+// acc + r*b (real r)
+__device__ __forceinline__ double2 rfma(double r, double2 b, double2 acc) {
+  return make_double2(__fma_rn(r, b.x, acc.x), __fma_rn(r, b.y, acc.y));
+}
+
 // Smith's complex division a / b (numpy's npy_cdiv algorithm).
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   const double abs_br = fabs(b.x), abs_bi = fabs(b.y);
@@ -34,6 +51,9 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -57,6 +77,18 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// x-vector loads.  NC = true: the launch never writes x, plain loads (the compiler may take the
+// read-only path).  NC = false: the persistent fused tick kernel writes x (P, X) in a later phase of
+// the same launch, so x is read with an explicit weak ld.global -- never the non-coherent path,
+// whose cache lives for the whole launch; the grid barrier's fences order it.
+template <bool NC>
+__device__ __forceinline__ double2 ldx(const double2* p) {
+  if (NC) return *p;
+  double2 v;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 
@@ -124,8 +156,7 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const double2 v = xb[d];
-      acc[d].x += a.x * v.x - am * v.y;
-      acc[d].y += a.x * v.y + am * v.x;
+      acc[d] = cfma(make_double2(a.x, am), v, acc[d]);
     }
   }
   const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
@@ -134,8 +165,7 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const double dv = __ldg(op.dp + (size_t)e * DIM + d);
-      acc[d].x += dv * v.x;
-      acc[d].y += dv * v.y;
+      acc[d] = rfma(dv, v, acc[d]);
     }
   }
 #pragma unroll
@@ -146,7 +176,7 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
 }
 
 // One warp computes pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
-template <int DIM>
+template <int DIM, bool NC = true>
 __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int j,
                                                    const double2* __restrict__ x, int lane, int xs = 1) {
   double2 acc = make_double2(0.0, 0.0);
@@ -157,9 +187,8 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const double dv = ldm(op.dt + (size_t)e * DIM + d);
-      const double2 v = xb[(size_t)d * xs];
-      acc.x += dv * v.x;
-      acc.y += dv * v.y;
+      const double2 v = ldx<NC>(xb + (size_t)d * xs);
+      acc = rfma(dv, v, acc);
     }
   }
   acc.x = warp_sum(acc.x);
@@ -168,6 +197,7 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
 }
 
 // Generic complex CSR row (drop-in gmres on arbitrary matrices): warp per row.
+template <bool NC = true>
 __device__ __forceinline__ double2 csr_row(const SsCsrDev& A, int set, int row,
                                            const double2* __restrict__ x, int lane) {
   double2 acc = make_double2(0.0, 0.0);
@@ -175,9 +205,8 @@ __device__ __forceinline__ double2 csr_row(const SsCsrDev& A, int set, int row,
   const int e0 = __ldg(A.indptr + row), e1 = __ldg(A.indptr + row + 1);
   for (int e = e0 + lane; e < e1; e += 32) {
     const double2 a = __ldg(vals + e);
-    const double2 v = x[__ldg(A.indices + e)];
-    acc.x += a.x * v.x - a.y * v.y;
-    acc.y += a.x * v.y + a.y * v.x;
+    const double2 v = ldx<NC>(x + __ldg(A.indices + e));
+    acc = cfma(a, v, acc);
   }
   acc.x = warp_sum(acc.x);
   acc.y = warp_sum(acc.y);
@@ -216,7 +245,7 @@ __device__ __forceinline__ int4 row_ranges(const SsOperatorDev& op, int r) {
   return make_int4(__ldg(op.nptr + r), __ldg(op.nptr + r + 1), __ldg(op.pptr + r), __ldg(op.pptr + r + 1));
 }
 
-template <int DIM>
+template <int DIM, bool NC = true>
 __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r, double omega,
                                                   const double2* __restrict__ x, int gl, double2 (&acc)[DIM],
                                                   int xs = 1) {
@@ -233,20 +262,18 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
       const double2* xb = x + (size_t)B * DIM * xs;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        const double2 v = xb[(size_t)d * xs];
-        acc[d].x += a.x * v.x - am * v.y;
-        acc[d].y += a.x * v.y + am * v.x;
+        const double2 v = ldx<NC>(xb + (size_t)d * xs);
+        acc[d] = cfma(make_double2(a.x, am), v, acc[d]);
       }
     }
     const int p0 = rg.z, p1 = rg.w;
 #pragma unroll 2
     for (int e = p0 + gl; e < p1; e += ROW_LANES) {
-      const double2 v = x[(size_t)(op.nfv + ldm(op.pcol + e)) * xs];
+      const double2 v = ldx<NC>(x + (size_t)(op.nfv + ldm(op.pcol + e)) * xs);
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         const double dv = ldm(op.dp + (size_t)e * DIM + d);
-        acc[d].x += dv * v.x;
-        acc[d].y += dv * v.y;
+        acc[d] = rfma(dv, v, acc[d]);
       }
     }
   }
@@ -260,7 +287,7 @@ __device__ __forceinline__ void saddle_vel_row_g8(const SsOperatorDev& op, int r
 }
 
 // x is read with stride xs (xs = batch: one mode's column of the mode-interleaved P).
-template <int DIM, class Emit>
+template <int DIM, bool NC = true, class Emit>
 __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, double omega,
                                              const double2* __restrict__ x, Emit&& emit, int xs = 1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -275,7 +302,7 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
       const int r = rbase + it * 8 * RPW;
       const bool ok = r < op.nfree;
       double2 acc[DIM];
-      saddle_vel_row_g8<DIM>(op, ok ? r : -1, omega, x, gl, acc, xs);
+      saddle_vel_row_g8<DIM, NC>(op, ok ? r : -1, omega, x, gl, acc, xs);
       if (ok && gl < DIM) {
         double2 v = acc[0];
 #pragma unroll
@@ -289,14 +316,14 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
     for (int it = 0; it < SPMV_PROWS / 8; ++it) {
       const int j = pb * SPMV_PROWS + it * 8 + warp;
       if (j < op.npf) {
-        const double2 v = saddle_pres_row<DIM>(op, j, x, lane, xs);
+        const double2 v = saddle_pres_row<DIM, NC>(op, j, x, lane, xs);
         if (lane == 0) emit(op.nfv + j, v);
       }
     }
   }
 }
 
-template <class Emit>
+template <bool NC = true, class Emit>
 __device__ __forceinline__ void csr_block(const SsCsrDev& A, int set, int blk, const double2* __restrict__ x,
                                           Emit&& emit) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -304,7 +331,7 @@ __device__ __forceinline__ void csr_block(const SsCsrDev& A, int set, int blk, c
   for (int it = 0; it < SPMV_PROWS / 8; ++it) {
     const int row = blk * SPMV_PROWS + it * 8 + warp;
     if (row < A.n) {
-      const double2 v = csr_row(A, set, row, x, lane);
+      const double2 v = csr_row<NC>(A, set, row, x, lane);
       if (lane == 0) emit(row, v);
     }
   }
@@ -316,6 +343,10 @@ __device__ __forceinline__ double2 ldnc2(const double2* p) {
   return v;
 }
 
+// P gathers of the mode-interleaved SpMV: non-coherent path unless the launch also writes P.
+template <bool NC>
+__device__ __forceinline__ double2 ldp2(const double2* p) { return NC ? ldnc2(p) : ldx<false>(p); }
+
 #ifndef SS_IL_UNROLL
 #define SS_IL_UNROLL 4
 #endif
@@ -326,7 +357,7 @@ constexpr int IL_U = SS_IL_UNROLL;   // node entries per load round of a (row, m
 // Threads walk the block's (row, mode) pairs, mode fastest: matrix loads are broadcasts and the
 // x gathers contiguous runs over the batch.  Each (row, mode) is summed by one thread in entry
 // order (deterministic, independent of the batch).  active(m) selects modes; scale(m) multiplies.
-template <int DIM, class Active, class Omega, class Scale>
+template <int DIM, bool NC = true, class Active, class Omega, class Scale>
 __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op, int blk, int sub, int split,
                                                          int nb, int ps, const double2* __restrict__ x,
                                                          double2* __restrict__ y, int64_t ld, int jacobi,
@@ -356,14 +387,13 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
 #pragma unroll
         for (int u = 0; u < IL_U; ++u)
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) v[u][d] = ldnc2(P + ((size_t)B[u] * DIM + d) * ps);
+          for (int d = 0; d < DIM; ++d) v[u][d] = ldp2<NC>(P + ((size_t)B[u] * DIM + d) * ps);
 #pragma unroll
         for (int u = 0; u < IL_U; ++u) {
           const double am = om * sm[u].y;
 #pragma unroll
           for (int d = 0; d < DIM; ++d) {
-            acc[d].x += sm[u].x * v[u][d].x - am * v[u][d].y;
-            acc[d].y += sm[u].x * v[u][d].y + am * v[u][d].x;
+            acc[d] = cfma(make_double2(sm[u].x, am), v[u][d], acc[d]);
           }
         }
       }
@@ -373,20 +403,18 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
         const double am = om * sm.y;
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          const double2 v = ldnc2(P + ((size_t)B * DIM + d) * ps);
-          acc[d].x += sm.x * v.x - am * v.y;
-          acc[d].y += sm.x * v.y + am * v.x;
+          const double2 v = ldp2<NC>(P + ((size_t)B * DIM + d) * ps);
+          acc[d] = cfma(make_double2(sm.x, am), v, acc[d]);
         }
       }
       const int p0 = __ldg(op.pptr + r), p1 = __ldg(op.pptr + r + 1);
 #pragma unroll 4
       for (int q = p0; q < p1; ++q) {
-        const double2 v = ldnc2(P + (size_t)(op.nfv + __ldg(op.pcol + q)) * ps);
+        const double2 v = ldp2<NC>(P + (size_t)(op.nfv + __ldg(op.pcol + q)) * ps);
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
           const double dv = __ldg(op.dp + (size_t)q * DIM + d);
-          acc[d].x += dv * v.x;
-          acc[d].y += dv * v.y;
+          acc[d] = rfma(dv, v, acc[d]);
         }
       }
       const double2 sj = jacobi ? saddle_jacobi(op, r, om) : make_double2(1.0, 0.0);
@@ -401,9 +429,8 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
           const double dv = __ldg(op.dt + (size_t)e * DIM + d);
-          const double2 v = ldnc2(xb + (size_t)d * ps);
-          acc.x += dv * v.x;
-          acc.y += dv * v.y;
+          const double2 v = ldp2<NC>(xb + (size_t)d * ps);
+          acc = rfma(dv, v, acc);
         }
       }
       w[op.nfv + r] = cscale(acc, xs);
@@ -530,8 +557,7 @@ __device__ __forceinline__ void saddle_stream(const SsOperatorDev& op, int nb, i
 #pragma unroll
           for (int d = 0; d < DIM; ++d) {
             const double2 v = xb[(size_t)d * xs];
-            acc[d].x += a.x * v.x - am * v.y;
-            acc[d].y += a.x * v.y + am * v.x;
+            acc[d] = cfma(make_double2(a.x, am), v, acc[d]);
           }
         }
 #pragma unroll 2
@@ -540,8 +566,7 @@ __device__ __forceinline__ void saddle_stream(const SsOperatorDev& op, int nb, i
 #pragma unroll
           for (int d = 0; d < DIM; ++d) {
             const double dv = sdp[(size_t)e * DIM + d];
-            acc[d].x += dv * v.x;
-            acc[d].y += dv * v.y;
+            acc[d] = rfma(dv, v, acc[d]);
           }
         }
 #pragma unroll
@@ -583,8 +608,7 @@ __device__ __forceinline__ void saddle_stream(const SsOperatorDev& op, int nb, i
             for (int d = 0; d < DIM; ++d) {
               const double dv = sdt[(size_t)e * DIM + d];
               const double2 v = xb[(size_t)d * xs];
-              acc.x += dv * v.x;
-              acc.y += dv * v.y;
+              acc = rfma(dv, v, acc);
             }
           }
           acc.x = warp_sum(acc.x);

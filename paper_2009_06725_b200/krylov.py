@@ -81,12 +81,12 @@ class KrylovWorkspace:
         self._finalizer()
 
     def set_option(self, name: str, value: int):
-        """Native workspace option (``ss_krylov_set_option``): "row_spmv", "device_loop", "ticks_per_graph"."""
+        """Native workspace option (``ss_krylov_set_option``): "row_spmv", "device_loop", "ticks_per_graph", "fused"."""
         _lib.call("ss_krylov_set_option", self._h, name.encode(), int(value))
 
     def options(self):
         out = {}
-        for name in ("row_spmv", "stream_spmv", "device_loop", "ticks_per_graph"):
+        for name in ("row_spmv", "stream_spmv", "device_loop", "ticks_per_graph", "fused", "fused_active"):
             v = C.c_int64()
             _lib.call("ss_krylov_get_option", self._h, name.encode(), C.byref(v))
             out[name] = int(v.value)
