@@ -112,3 +112,36 @@ def test_concurrent_gmres_solve_equals_sequential():
     for (xa, ra), (xb, rb) in zip(seq, par):
         assert np.array_equal(xa, xb)
         assert ra.iterations == rb.iterations and ra.residual == rb.residual
+
+
+@pytest.mark.parametrize("which", ["c1", "pipe3d", "c1_wide"])
+def test_fused_tick_bitwise_equals_kernel_tick(which):
+    """The persistent fused tick (one cooperative launch per ticks_per_graph ticks, grid barriers
+    between the SpMV / A / B / C phases) makes the same sums in the same order as the four-kernel
+    graphed tick: iterations, histories and solutions are bitwise equal (and converged fields match
+    the reference)."""
+    if which == "pipe3d":
+        case, idx, restart, maxiter = pipe3d_case(), [1, 16], 200, 200_000
+    else:
+        case, idx = c1_case(), [1, 4, 7]
+        restart, maxiter = (200, 200_000) if which == "c1" else (300, 700)
+    props = FluidProps(case.density, case.viscosity)
+    op = get_operator(case.qmesh, props)
+    settings = SolverSettings(tolerance=C1_TOL, restart=restart, max_iterations=maxiter)
+    g = None if case.kind != "dirichlet" else [case.coefficients[i] * case.profile for i in idx]
+    h = None if case.kind != "neumann" else [case.h_modes()[i] for i in idx]
+    runs = {}
+    for fused in (0, 1):
+        with workspace_option(op, restart, len(idx), maxiter, "fused", fused) as ws:
+            runs[fused] = solve_mode_systems(case.qmesh, props, idx, case.omegas[idx], g, h, settings)
+            if fused:
+                assert ws.options()["fused_active"] == 1
+    for a, b in zip(runs[0], runs[1]):
+        assert a.report.iterations == b.report.iterations
+        assert a.report.residual_history == b.report.residual_history
+        assert np.array_equal(a.velocity, b.velocity) and np.array_equal(a.pressure, b.pressure)
+    if which == "pipe3d":
+        ref = golden("pipe3d.npz")
+        for s in runs[1]:
+            assert s.report.converged
+            assert _rel(s.velocity, ref[f"u_{s.index}"]) <= 1e-7
