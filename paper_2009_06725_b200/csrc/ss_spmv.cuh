@@ -176,13 +176,24 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
 }
 
 // One warp computes pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
-template <int DIM, bool NC = true>
+// Lanes per pressure row of the row-layout SpMV (32: a warp per row; 8 or 16: 4 or 2 rows per warp;
+// the 32-row pressure blocks need >= 8).  Config 5 in-cycle: 32 lanes 3.83 ms, 16 3.82, 8 3.66.
+#ifndef SS_PRES_LANES
+#define SS_PRES_LANES 8
+#endif
+constexpr int PRES_LANES = SS_PRES_LANES;
+
+// PL lanes (an aligned group) compute pressure row j (j < 0: contributes nothing; every lane of
+// the warp must call, the group reduction is an xor butterfly over PL lanes).
+template <int DIM, bool NC = true, int PL = 32>
 __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int j,
                                                    const double2* __restrict__ x, int lane, int xs = 1) {
   double2 acc = make_double2(0.0, 0.0);
-  const int e0 = __ldg(op.tptr + j), e1 = __ldg(op.tptr + j + 1);
+  int e0 = 0, e1 = 0;
+  if (j >= 0) { e0 = __ldg(op.tptr + j); e1 = __ldg(op.tptr + j + 1); }
+  const int gl = lane % PL;
 #pragma unroll PRES_UNROLL
-  for (int e = e0 + lane; e < e1; e += 32) {
+  for (int e = e0 + gl; e < e1; e += PL) {
     const double2* xb = x + (size_t)ldm(op.tcol + e) * DIM * xs;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
@@ -191,8 +202,11 @@ __device__ __forceinline__ double2 saddle_pres_row(const SsOperatorDev& op, int 
       acc = rfma(dv, v, acc);
     }
   }
-  acc.x = warp_sum(acc.x);
-  acc.y = warp_sum(acc.y);
+#pragma unroll
+  for (int o = PL / 2; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
   return acc;
 }
 
@@ -229,13 +243,14 @@ __device__ __host__ __forceinline__ int saddle_nsb_host(int nfree, int npf) {
   return (nfree + SPMV_VROWS - 1) / SPMV_VROWS + (npf + SPMV_PROWS - 1) / SPMV_PROWS;
 }
 
-// Lanes per node row of the row-layout SpMV (8: four rows per warp; 16: two).
+// Lanes per node row of the row-layout SpMV (4: eight rows per warp).  Config 5 in-cycle (unroll):
+// 8 lanes (8) 4.33 ms, 4 lanes (4) 3.80, (2) 4.04, (6) 4.26, 2 lanes (4 / 8) 4.45 / 4.59 (80 registers).
 #ifndef SS_ROW_LANES
-#define SS_ROW_LANES 8
+#define SS_ROW_LANES 4
 #endif
 constexpr int ROW_LANES = SS_ROW_LANES;
 #ifndef SS_ROW_UNROLL
-#define SS_ROW_UNROLL 8
+#define SS_ROW_UNROLL 4
 #endif
 constexpr int ROW_UNROLL = SS_ROW_UNROLL;   // node entries of a lane's row loaded per loop round
 
@@ -303,22 +318,29 @@ __device__ __forceinline__ void saddle_block(const SsOperatorDev& op, int blk, d
       const bool ok = r < op.nfree;
       double2 acc[DIM];
       saddle_vel_row_g8<DIM, NC>(op, ok ? r : -1, omega, x, gl, acc, xs);
-      if (ok && gl < DIM) {
-        double2 v = acc[0];
+      if constexpr (ROW_LANES >= DIM) {
+        if (ok && gl < DIM) {
+          double2 v = acc[0];
 #pragma unroll
-        for (int d = 1; d < DIM; ++d) if (gl == d) v = acc[d];
-        emit(r * DIM + gl, v);
+          for (int d = 1; d < DIM; ++d) if (gl == d) v = acc[d];
+          emit(r * DIM + gl, v);
+        }
+      } else if (ok) {   // fewer lanes than components: lane gl emits components gl, gl + ROW_LANES, ...
+#pragma unroll
+        for (int d = 0; d < DIM; ++d)
+          if (d % ROW_LANES == gl) emit(r * DIM + d, acc[d]);
       }
     }
   } else {
     const int pb = blk - nvb;
+    constexpr int PRPW = 32 / PRES_LANES;   // pressure rows per warp per iteration
+    static_assert(SPMV_PROWS % (8 * PRPW) == 0 && SPMV_PROWS >= 8 * PRPW, "pressure block must cover whole warps");
 #pragma unroll 1
-    for (int it = 0; it < SPMV_PROWS / 8; ++it) {
-      const int j = pb * SPMV_PROWS + it * 8 + warp;
-      if (j < op.npf) {
-        const double2 v = saddle_pres_row<DIM, NC>(op, j, x, lane, xs);
-        if (lane == 0) emit(op.nfv + j, v);
-      }
+    for (int it = 0; it < SPMV_PROWS / (8 * PRPW); ++it) {
+      const int j = pb * SPMV_PROWS + (it * 8 + warp) * PRPW + lane / PRES_LANES;
+      const bool ok = j < op.npf;
+      const double2 v = saddle_pres_row<DIM, NC, PRES_LANES>(op, ok ? j : -1, x, lane, xs);
+      if (ok && lane % PRES_LANES == 0) emit(op.nfv + j, v);
     }
   }
 }
