@@ -585,7 +585,7 @@ def _spmv_numbers(op, omegas, ws, e0, e1, stream, hbm_peak, torch):
     row = ws.options()["row_spmv"]
     if row:
         ms = time_it(lambda: op.spmv(omegas, xr, jacobi=True, out=ys))
-        kern = "row-layout tick SpMV (saddle_block: 8 lanes per node row)"
+        kern = "row-layout tick SpMV (saddle_block: 4 lanes per node row, 8 per pressure row)"
     else:
         xi = torch.randn((op.ld, nb), dtype=torch.complex128, device=op.device)
         ms = time_it(lambda: op.spmv_interleaved(omegas, xi, jacobi=True, out=ys))
