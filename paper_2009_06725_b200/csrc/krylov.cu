@@ -84,6 +84,7 @@ struct KArgs {
   int wide;                    // restart > WIDE_RESTART: basis passes without the shared-memory ring (any J)
   int stream_spmv;             // row layout: TMA-staged persistent SpMV (1) or one CTA per row block (0)
   int fused;                   // running inside k_tick_fused (persistent, grid barriers between phases)
+  int ahead_bytes;             // basis-pass prefetch cap (bytes in flight per CTA; 0 = the whole ring)
   long long* ptime;            // fused-kernel phase timestamps [tick % FUSED_PROF_TICKS][5] (SS_FUSED_PROF)
 };
 constexpr int FUSED_PROF_TICKS = 1 << 16;
@@ -456,6 +457,15 @@ enum PassKind : int { PASS_A = 1, PASS_B = 2, PASS_C = 3, PASS_X = 4 };
 
 // TMA bulk-copy / mbarrier helpers: ss_spmv.cuh
 
+// Chunks kept in flight ahead of the consumer: the ring's NS - 1, capped at a.ahead_bytes (bulk
+// reads stream fastest with ~50-100 KB in flight per SM, tools/probes/read_bw.cu); never below
+// one.  Only the issue time of the copies changes, not the chunking: sums are unaffected.
+__device__ __forceinline__ int pass_ahead(const KArgs& a, int NS, int stage_elems) {
+  int ah = NS - 1;
+  if (a.ahead_bytes > 0) ah = min(ah, max(1, a.ahead_bytes / (stage_elems * 16)));
+  return max(ah, NS > 1 ? 1 : 0);
+}
+
 __device__ __forceinline__ int pass_slices(int nr) { return nr > 4 ? 1 : nr > 2 ? 2 : nr > 1 ? 4 : 8; }
 
 // Streams one segment (SEGB row blocks) of one mode's basis through a ring of shared-memory
@@ -478,6 +488,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   const int CB = PASS == PASS_B ? 1 : max(1, min(min(nblocks, 8), (a.smem_elems / div) / (belem + RB)));
   const int stage_elems = CB * (belem + RB);
   const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
+  const int AH = pass_ahead(a, NS, stage_elems);
   const int nchunks = (nblocks + CB - 1) / CB;
   double2* vec = (PASS == PASS_X ? a.X : a.W) + (size_t)b * a.ld;
   auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
@@ -494,13 +505,13 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   fence_mbar_init();
   __syncthreads();
   if (tid == 0)
-    for (int ci = 0; ci < NS - 1 && ci < nchunks; ++ci) load_chunk(ci);
+    for (int ci = 0; ci < AH && ci < nchunks; ++ci) load_chunk(ci);
   double2 acc[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
   double nrm = 0.0;
   for (int ci = 0; ci < nchunks; ++ci) {
-    if (tid == 0 && ci + NS - 1 < nchunks) load_chunk(ci + NS - 1);   // stage of chunk ci-1 (released)
+    if (tid == 0 && ci + AH < nchunks) load_chunk(ci + AH);   // stage of chunk ci+AH-NS <= ci-1 (released)
     mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
     double2* st = stage(ci);
     const int c0 = blk_begin + ci * CB;
@@ -724,6 +735,7 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
   const int CB = min(NG, nblocks);
   const int stage_elems = CB * blk_elems;
   const int NS = max(1, min(PASS_MAX_STAGES, a.smem_elems / stage_elems));
+  const int AH = pass_ahead(a, NS, stage_elems);
   const int nchunks = (nblocks + CB - 1) / CB;
   double2* vec = a.W + (size_t)b * a.ld;
   auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
@@ -740,13 +752,13 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
   fence_mbar_init();
   __syncthreads();
   if (tid == 0)
-    for (int ci = 0; ci < NS - 1 && ci < nchunks; ++ci) load_chunk(ci);
+    for (int ci = 0; ci < AH && ci < nchunks; ++ci) load_chunk(ci);
   double2 acc[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
   int bi = 0;
   for (int ci = 0; ci < nchunks; ++ci) {
-    if (tid == 0 && ci + NS - 1 < nchunks) load_chunk(ci + NS - 1);   // stage of chunk ci-1 (released)
+    if (tid == 0 && ci + AH < nchunks) load_chunk(ci + AH);   // stage of chunk ci+AH-NS <= ci-1 (released)
     mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
     const double2* st = stage(ci);
     const int c0 = blk_begin + ci * CB;
@@ -1216,6 +1228,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if (!a.wide) a.smem_elems = std::max(a.smem_elems, a.jcap * RB + 2 * RB);   // one full-J block + vector must fit a stage
   else a.smem_elems = 3 * 256;                                                  // no ring; pass C staging unused
   if (const char* e = getenv("SS_PASS_DIV")) a.stage_div = std::max(1, atoi(e));
+  a.ahead_bytes = 0;
+  if (const char* e = getenv("SS_PASS_AHEAD")) a.ahead_bytes = std::max(0, atoi(e));
   K->max_batch = max_batch;
   const size_t B = max_batch;
   int rc;
