@@ -1213,7 +1213,10 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   // segment rows depend on n only (batch-composition invariance of every reduction): ~16 segments
   // for small n (config 1: one wave of CTAs for 9 modes, +25 %), 6144 rows for large n (config 2:
   // 2 210 CTAs = 14.9 waves of 148 for 17 modes; 4096 and 8192 measured 1 % slower)
-  int64_t segdiv = 16, segmin = 256, segmax = 6144;
+  // 2D saddle systems: ~24 segments (config 1 through the concurrent sub-batches: 14.96 vs 13.82
+  // modes/s; 3D at the same n -- pipe3d -- stays best at 16: 5.11 vs 4.96).  A rule on the system
+  // (n, dim), never on the batch, so per-mode results stay batch-invariant.
+  int64_t segdiv = (K->a.kind == 0 && K->a.op.dim == 2) ? 24 : 16, segmin = 256, segmax = 6144;
   if (const char* e = getenv("SS_SEG_DIV")) segdiv = std::max(1, atoi(e));
   if (const char* e = getenv("SS_SEG_MIN")) segmin = std::max(32, atoi(e));
   if (const char* e = getenv("SS_SEG_MAX")) segmax = std::max(64, atoi(e));

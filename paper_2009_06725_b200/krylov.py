@@ -10,6 +10,7 @@ device-resident restarted GMRES with the reference's CGS2 + Givens + true-residu
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -334,7 +335,9 @@ def concurrent_groups(n: int, nb: int) -> int:
     +4 %).  Per-mode results are bitwise independent of the grouping (batch invariance)."""
     if n >= 200_000:
         return 1
-    return max(1, min(4, nb // 3))   # sub-batches of >= 3 modes (config 1: 4 groups of 2-3 measured -13 %)
+    k = max(1, min(4, nb // 3))   # sub-batches of >= 3 modes (config 1: 4 groups of 2-3 measured -13 %)
+    env = os.environ.get("SS_CONCURRENT_GROUPS")   # A/B knob (tools/c1_public_ab.py)
+    return max(1, min(nb, int(env))) if env else k
 
 
 def _solve_concurrent(op, batch, x0, settings, jac, hist_cap, keep_history, k):
