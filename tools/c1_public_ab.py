@@ -18,7 +18,7 @@ props = FluidProps(case.density, case.viscosity)
 op = get_operator(case.qmesh, props)
 b = assemble_mode_systems(case.qmesh, props, case.omegas, case.g_modes(), case.h_modes(), operator=op)
 st = SolverSettings(tolerance=1e-10, restart=200, max_iterations=400000)
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     X, reps = gmres_batched(b, st, keep_history=False)
