@@ -335,6 +335,8 @@ def concurrent_groups(n: int, nb: int) -> int:
     +4 %).  Per-mode results are bitwise independent of the grouping (batch invariance)."""
     if n >= 200_000:
         return 1
+    if os.environ.get("SS_FUSED", "0") not in ("", "0"):
+        return 1   # persistent cooperative tick kernels occupy every SM: never two at once
     k = max(1, min(4, nb // 3))   # sub-batches of >= 3 modes (config 1: 4 groups of 2-3 measured -13 %)
     env = os.environ.get("SS_CONCURRENT_GROUPS")   # A/B knob (tools/c1_public_ab.py)
     return max(1, min(nb, int(env))) if env else k
