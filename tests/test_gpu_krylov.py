@@ -390,3 +390,33 @@ def test_maximum_batch_with_zero_and_steady_modes(small_channel_qmesh, fluid):
     for b in range(5, nb, 31):
         assert reps[b].iterations == 0 and reps[b].converged and not np.any(X[b])
     assert all(r.converged for r in reps)
+
+
+def test_zero_denominator_breakdown_matches_oracle():
+    """A x = b with A = 0 (explicit zeros): w = 0, h_kk = h_{k+1,k} = 0, so the Givens denominator is
+    0 -- the reference's breakdown branch (krylov.py:124-129): one iteration counted, no update, not
+    converged, x = 0 (and the true residual 1)."""
+    n = 12
+    a = sp.csr_matrix((np.zeros(n, complex), np.arange(n), np.arange(n + 1)), shape=(n, n))
+    b = np.arange(1, n + 1) + 0.5j
+    x, it, hist, conv = gmres(a, b, tol=1e-10, restart=5, maxiter=50)
+    xo, io, ho, co = oracle.gmres(a, b, 1e-10, 5, 50)
+    assert it == io == 1 and not conv and not co
+    assert hist == ho == []
+    assert np.all(x == 0) and np.all(xo == 0)
+
+
+@pytest.mark.parametrize("n", [1, 37])
+def test_restart_one_and_tiny_systems_match_oracle(n):
+    """GMRES(1) (every iteration a cycle end) and a 1x1 system, against the oracle iteration."""
+    rng = np.random.default_rng(40 + n)
+    a = sp.csr_matrix(_random_complex_symmetric(n, rng))
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    sc = oracle.jacobi_scale(a)
+    x, it, hist, conv = gmres(a, b, tol=1e-11, restart=1, maxiter=400, scale=sc)
+    xo, io, ho, co = oracle.gmres(a, b, 1e-11, 1, 400, scale=sc)
+    assert it == io and conv == co
+    # estimates agree to rounding relative to the initial (preconditioned) residual norm: the last
+    # ones sit at 1e-13 of it (n = 37), or at the 1e-32 noise floor of an exact 1-step solve (n = 1)
+    np.testing.assert_allclose(hist, ho, rtol=1e-6, atol=1e-10 * np.linalg.norm(sc * b))
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
