@@ -175,7 +175,7 @@ __device__ __forceinline__ void saddle_vel_row(const SsOperatorDev& op, int r, d
   }
 }
 
-// One warp computes pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
+// Pressure row j: sum over free nodes B, components d of D[(B,d),P] x_(B,d).
 // Lanes per pressure row of the row-layout SpMV (32: a warp per row; 8 or 16: 4 or 2 rows per warp;
 // the 32-row pressure blocks need >= 8).  Config 5 in-cycle: 32 lanes 3.83 ms, 16 3.82, 8 3.66.
 #ifndef SS_PRES_LANES
@@ -466,9 +466,11 @@ __device__ __forceinline__ void saddle_block_interleaved(const SsOperatorDev& op
 // is moved into a shared-memory stage by bulk copies (cp.async.bulk + mbarrier, a ring of
 // STREAM_STAGES stages filled STREAM_STAGES-1 chunks ahead), so the only global loads left in the
 // compute loop are the x gathers; the staged chunk is then applied to every active mode.  The
-// per-row arithmetic is that of saddle_vel_row_g8 / saddle_pres_row (8 lanes per node row with
-// the same entry assignment and xor-shuffle tree; a warp per pressure row), so results equal the
-// row-layout saddle_block's.  Chunks (built on the host, pattern.cpp) never exceed one stage.
+// per-row arithmetic is that of saddle_vel_row_g8 / saddle_pres_row with 8 lanes per node row and
+// a warp per pressure row (results equal the row-layout saddle_block's when it is built with
+// SS_ROW_LANES=8, SS_PRES_LANES=32; the default row layout now uses 4 / 8 lanes, so the two agree
+// to rounding).  Off by default (measured slower).  Chunks (built on the host,
+// pattern.cpp) never exceed one stage.
 // ------------------------------------------------------------------------------------------------
 constexpr int STREAM_STAGE_BYTES = 32768;
 constexpr int STREAM_STAGES = 3;
