@@ -135,7 +135,9 @@ void ss_krylov_destroy(ss_krylov* k);
 int ss_krylov_info(const ss_krylov* k, int64_t* info);
 /* Workspace option (drops cached graphs): "row_spmv" (0/1: mode-interleaved or row-layout tick
  * SpMV; default by n), "stream_spmv" (0/1: row layout through the TMA-staged persistent kernel),
- * "device_loop" (0/1), "ticks_per_graph" (1..1024).  Results never depend on
+ * "device_loop" (0/1), "ticks_per_graph" (1..1024), "fused" (0/1: persistent cooperative tick),
+ * "pass_alt" (0/1: basis passes stream their segments in alternating directions, for L2 reuse
+ * between consecutive passes; changes the order of the passes' row sums).  Results never depend on
  * ticks_per_graph/device_loop; the SpMV layout changes no per-row summation order either. */
 int ss_krylov_set_option(ss_krylov* k, const char* name, int64_t value);
 /* Current value of a workspace option (names as for ss_krylov_set_option). */

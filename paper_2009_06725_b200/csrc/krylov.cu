@@ -86,6 +86,7 @@ struct KArgs {
   int fused;                   // running inside k_tick_fused (persistent, grid barriers between phases)
   int row_dyn;                 // row-layout tick SpMV: blocks dealt from an atomic counter (SS_ROW_DYN)
   int ahead_bytes;             // basis-pass prefetch cap (bytes in flight per CTA; 0 = the whole ring)
+  int pass_alt;                // basis passes stream their segment in alternating directions (SS_PASS_ALT)
   long long* ptime;            // fused-kernel phase timestamps [tick % FUSED_PROF_TICKS][5] (SS_FUSED_PROF)
 };
 constexpr int FUSED_PROF_TICKS = 1 << 16;
@@ -496,7 +497,8 @@ __device__ __forceinline__ int pass_slices(int nr) { return nr > 4 ? 1 : nr > 2 
 // Writes this CTA's partials: part[j] (A, B) or part[0].x = ||w||^2 (C).
 template <int PASS, int T>
 __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int J, int k, const double2* coef,
-                                               double2* smem, uint64_t* mbar, double2* red, double2* part) {
+                                               double2* smem, uint64_t* mbar, double2* red, double2* part,
+                                               bool rev = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int segb = a.seg_rows / RB;
   const int blk_begin = s * segb;
@@ -515,7 +517,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
   auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
   auto load_chunk = [&](int ci) {   // single producer thread
     double2* st = stage(ci);
-    const int c0 = blk_begin + ci * CB;
+    const int c0 = blk_begin + (rev ? nchunks - 1 - ci : ci) * CB;
     const int nc = min(CB, blk_end - c0);
     uint64_t* bar = &mbar[ci % NS];
     mbar_expect_tx(bar, (unsigned)(nc * (belem + RB) * 16));
@@ -535,7 +537,7 @@ __device__ __forceinline__ void stream_segment(const KArgs& a, int b, int s, int
     if (tid == 0 && ci + AH < nchunks) load_chunk(ci + AH);   // stage of chunk ci+AH-NS <= ci-1 (released)
     mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
     double2* st = stage(ci);
-    const int c0 = blk_begin + ci * CB;
+    const int c0 = blk_begin + (rev ? nchunks - 1 - ci : ci) * CB;
     const int nc = min(CB, blk_end - c0);
     double2* Vb = st + CB * belem;
     if (PASS == PASS_B) {
@@ -741,7 +743,7 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 // Same two phases as stream_segment<PASS_B>: w -= sum_j q_j c_j, then acc_t += conj(q_j) w, with
 // the block's basis values held in registers between them.
 template <int G, int T>
-__device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, int J, const double2* coef,
+__device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, int J, bool rev, const double2* coef,
                                                   double2* smem, uint64_t* mbar, double2* red, double2* part) {
   constexpr int NG = 8 / G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -762,7 +764,7 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
   auto stage = [&](int ci) { return smem + (size_t)(ci % NS) * stage_elems; };
   auto load_chunk = [&](int ci) {   // single producer thread
     double2* st = stage(ci);
-    const int c0 = blk_begin + ci * CB;
+    const int c0 = blk_begin + (rev ? nchunks - 1 - ci : ci) * CB;
     const int nc = min(CB, blk_end - c0);
     uint64_t* bar = &mbar[ci % NS];
     mbar_expect_tx(bar, (unsigned)(nc * blk_elems * 16));
@@ -782,7 +784,7 @@ __device__ __forceinline__ void stream_segment_bg(const KArgs& a, int b, int s, 
     if (tid == 0 && ci + AH < nchunks) load_chunk(ci + AH);   // stage of chunk ci+AH-NS <= ci-1 (released)
     mbar_wait(&mbar[ci % NS], (unsigned)((ci / NS) & 1));
     const double2* st = stage(ci);
-    const int c0 = blk_begin + ci * CB;
+    const int c0 = blk_begin + (rev ? nchunks - 1 - ci : ci) * CB;
     const int nc = min(CB, blk_end - c0);
     const double2* Vb = st + CB * belem;
     if (grp < nc) {
@@ -888,6 +890,10 @@ __device__ __forceinline__ void pass_body(const KArgs& a, int vb, double2* smem,
   double* qs = a.qs + (size_t)b * a.jcap;
   double2* part = a.part + (size_t)b * a.nseg * a.jcap + (size_t)s * a.jcap;
   const int T = (J + 7) / 8;
+  // Streaming direction (SS_PASS_ALT): A and C forward on even k, B the other way, all flipped on
+  // odd k, so every pass starts on the rows its predecessor read last (still in L2 when the
+  // batch's basis is not much larger than L2).  Depends only on this mode's k: batch-invariant.
+  const bool rev = a.pass_alt && (((k & 1) != 0) != (PASS == PASS_B));
   if (a.wide) {
     stream_segment_wide<PASS>(a, b, s, J, k, red, part);
   } else {
@@ -901,23 +907,23 @@ __device__ __forceinline__ void pass_body(const KArgs& a, int vb, double2* smem,
   __syncthreads();
   if (PASS == PASS_B && J <= a.gthr[2]) {
     if (J <= a.gthr[0]) {
-      if (J <= 4) stream_segment_bg<1, 4>(a, b, s, J, coef, smem, mbar, red, part);
-      else if (J <= 8) stream_segment_bg<1, 8>(a, b, s, J, coef, smem, mbar, red, part);
-      else stream_segment_bg<1, 16>(a, b, s, J, coef, smem, mbar, red, part);
+      if (J <= 4) stream_segment_bg<1, 4>(a, b, s, J, rev, coef, smem, mbar, red, part);
+      else if (J <= 8) stream_segment_bg<1, 8>(a, b, s, J, rev, coef, smem, mbar, red, part);
+      else stream_segment_bg<1, 16>(a, b, s, J, rev, coef, smem, mbar, red, part);
     } else if (J <= a.gthr[1]) {
-      stream_segment_bg<2, 16>(a, b, s, J, coef, smem, mbar, red, part);
+      stream_segment_bg<2, 16>(a, b, s, J, rev, coef, smem, mbar, red, part);
     } else {
-      stream_segment_bg<4, 16>(a, b, s, J, coef, smem, mbar, red, part);
+      stream_segment_bg<4, 16>(a, b, s, J, rev, coef, smem, mbar, red, part);
     }
   } else if (PASS == PASS_A || PASS == PASS_B) {
-    if (T <= 2) stream_segment<PASS, 2>(a, b, s, J, k, coef, smem, mbar, red, part);
-    else if (T <= 4) stream_segment<PASS, 4>(a, b, s, J, k, coef, smem, mbar, red, part);
-    else if (T <= 8) stream_segment<PASS, 8>(a, b, s, J, k, coef, smem, mbar, red, part);
-    else if (T <= 16) stream_segment<PASS, 16>(a, b, s, J, k, coef, smem, mbar, red, part);
-    else if (T <= 26) stream_segment<PASS, 26>(a, b, s, J, k, coef, smem, mbar, red, part);
-    else stream_segment<PASS, 32>(a, b, s, J, k, coef, smem, mbar, red, part);
+    if (T <= 2) stream_segment<PASS, 2>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
+    else if (T <= 4) stream_segment<PASS, 4>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
+    else if (T <= 8) stream_segment<PASS, 8>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
+    else if (T <= 16) stream_segment<PASS, 16>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
+    else if (T <= 26) stream_segment<PASS, 26>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
+    else stream_segment<PASS, 32>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
   } else {
-    stream_segment<PASS, 1>(a, b, s, J, k, coef, smem, mbar, red, part);
+    stream_segment<PASS, 1>(a, b, s, J, k, coef, smem, mbar, red, part, rev);
   }
   }   // !a.wide
   if (PASS == PASS_X) {
@@ -1254,6 +1260,8 @@ static int krylov_common_init(ss_krylov* K, int n, int max_batch, int restart, i
   if (const char* e = getenv("SS_PASS_DIV")) a.stage_div = std::max(1, atoi(e));
   a.ahead_bytes = 0;
   if (const char* e = getenv("SS_PASS_AHEAD")) a.ahead_bytes = std::max(0, atoi(e));
+  a.pass_alt = 0;
+  if (const char* e = getenv("SS_PASS_ALT")) a.pass_alt = atoi(e) != 0;
   K->max_batch = max_batch;
   const size_t B = max_batch;
   int rc;
@@ -1441,6 +1449,8 @@ extern "C" int ss_krylov_set_option(ss_krylov* K, const char* name, int64_t valu
     K->ticks_per_graph = (int)value;
   } else if (opt == "fused") {
     K->fused = value ? 1 : 0;
+  } else if (opt == "pass_alt") {
+    K->a.pass_alt = value ? 1 : 0;
   } else {
     ss_set_error("unknown workspace option '" + opt + "'");
     return SS_ERR_ARG;
@@ -1459,6 +1469,7 @@ extern "C" int ss_krylov_get_option(const ss_krylov* K, const char* name, int64_
   else if (opt == "device_loop") *value = K->device_loop;
   else if (opt == "ticks_per_graph") *value = K->ticks_per_graph;
   else if (opt == "fused") *value = K->fused;
+  else if (opt == "pass_alt") *value = K->a.pass_alt;
   else if (opt == "fused_active") *value = K->fused && !(K->a.kind == 0 && K->a.row_spmv) && K->fused_grid >= 0;
   else { ss_set_error("unknown workspace option '" + opt + "'"); return SS_ERR_ARG; }
   return SS_OK;

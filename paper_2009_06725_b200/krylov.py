@@ -82,12 +82,12 @@ class KrylovWorkspace:
         self._finalizer()
 
     def set_option(self, name: str, value: int):
-        """Native workspace option (``ss_krylov_set_option``): "row_spmv", "device_loop", "ticks_per_graph", "fused"."""
+        """Native workspace option (``ss_krylov_set_option``): "row_spmv", "device_loop", "ticks_per_graph", "fused", "pass_alt"."""
         _lib.call("ss_krylov_set_option", self._h, name.encode(), int(value))
 
     def options(self):
         out = {}
-        for name in ("row_spmv", "stream_spmv", "device_loop", "ticks_per_graph", "fused", "fused_active"):
+        for name in ("row_spmv", "stream_spmv", "device_loop", "ticks_per_graph", "fused", "fused_active", "pass_alt"):
             v = C.c_int64()
             _lib.call("ss_krylov_get_option", self._h, name.encode(), C.byref(v))
             out[name] = int(v.value)

@@ -145,3 +145,46 @@ def test_fused_tick_bitwise_equals_kernel_tick(which):
         for s in runs[1]:
             assert s.report.converged
             assert _rel(s.velocity, ref[f"u_{s.index}"]) <= 1e-7
+
+
+def test_alternating_pass_direction_fixed_budget_matches_reference():
+    """Option "pass_alt" (basis passes stream their segments forward / backward by the parity of k,
+    for L2 reuse between consecutive passes) changes only the order of the passes' row sums: the
+    fixed-budget history and iterate still match the reference (c1, tests/golden/c1.npz)."""
+    case = c1_case()
+    props = FluidProps(case.density, case.viscosity)
+    g = golden("c1.npz")
+    s = assemble_mode_system(case.qmesh, props, case.omegas[1], h_mode=case.h_modes()[1])
+    with workspace_option(s.operator, 200, 1, 200, "pass_alt", 1):
+        x, rep = gmres_solve(s, SolverSettings(tolerance=C1_TOL, restart=200, max_iterations=200))
+    assert rep.iterations == 200
+    np.testing.assert_allclose(rep.residual_history, g["budget_hist"], rtol=1e-6)
+    assert _rel(x, g["budget_x"]) <= 1e-8
+
+
+def test_alternating_pass_direction_converged_batch_invariant_and_fused():
+    """pass_alt on the 3D pipe: converged fields within 1e-7 of the reference, bitwise equal between
+    a two-mode batch and a one-mode batch (the direction depends only on the mode's own k) and
+    between the four-kernel and the persistent fused tick."""
+    case, ref, idx = pipe3d_case(), golden("pipe3d.npz"), [1, 16]
+    props = FluidProps(case.density, case.viscosity)
+    op = get_operator(case.qmesh, props)
+    settings = SolverSettings(tolerance=C1_TOL, restart=200)
+    g = [case.coefficients[i] * case.profile for i in idx]
+    runs = {}
+    for fused in (0, 1):
+        with workspace_option(op, 200, len(idx), settings.max_iterations, "pass_alt", 1), \
+                workspace_option(op, 200, len(idx), settings.max_iterations, "fused", fused):
+            runs[fused] = solve_mode_systems(case.qmesh, props, idx, case.omegas[idx], g, None, settings)
+    with workspace_option(op, 200, 1, settings.max_iterations, "pass_alt", 1):
+        one = solve_mode_systems(case.qmesh, props, idx[1:], case.omegas[idx[1:]], g[1:], None, settings)
+    for a, b in zip(runs[0], runs[1]):
+        assert a.report.iterations == b.report.iterations
+        assert a.report.residual_history == b.report.residual_history
+        assert np.array_equal(a.velocity, b.velocity) and np.array_equal(a.pressure, b.pressure)
+    assert runs[0][1].report.iterations == one[0].report.iterations
+    assert np.array_equal(runs[0][1].velocity, one[0].velocity)
+    for s in runs[0]:
+        assert s.report.converged and s.report.residual <= C1_TOL
+        assert _rel(s.velocity, ref[f"u_{s.index}"]) <= 1e-7
+        assert _rel(s.pressure, ref[f"p_{s.index}"]) <= 1e-7
