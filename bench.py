@@ -615,12 +615,16 @@ def _converged_extras(torch):
         b = assemble_mode_systems(case.qmesh, props, case.omegas, case.g_modes(), case.h_modes(), operator=op)
         gmres_batched(b, settings, keep_history=False)   # warm-up (workspaces, graph capture)
         torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        X, reps = gmres_batched(b, settings, keep_history=False)
-        torch.cuda.synchronize()
-        sec = time.perf_counter() - w0
+        secs = []
+        for _ in range(1 if tag == "c3d_converged_c5small" else 3):   # sub-second solves: median of 3
+            w0 = time.perf_counter()
+            X, reps = gmres_batched(b, settings, keep_history=False)
+            torch.cuda.synchronize()
+            secs.append(time.perf_counter() - w0)
+        sec = sorted(secs)[len(secs) // 2]
         out[tag] = {"workload": case.name, "n_dofs": op.n, "modes": int(nm), "tol": TOL, "restart": RESTART,
-                    "seconds": sec, "modes_per_s": nm / sec, "all_converged": all(r.converged for r in reps),
+                    "seconds": sec, "repeat_seconds": secs, "modes_per_s": nm / sec,
+                    "all_converged": all(r.converged for r in reps),
                     "iterations": [int(r.iterations) for r in reps],
                     "concurrent_sub_batches": concurrent_groups(op.n, nm),
                     "measured": "every mode solved to the reference's stopping rule (true residual re-checked)"}
